@@ -1,0 +1,187 @@
+// K1: pilot sum-kernel Gram matrix (replaces the per-step window
+// re-evaluation of ApsmTrainer._window_response, apsm.py:288-302).
+//
+// One thread computes the 2x2 realified block of one (pilot p, pilot q) pair
+// from complex arithmetic (apsm.py:156-182 realification):
+//   r1(x).r1(y) = r2(x).r2(y) = Re(x^H y),  r1(x).r2(y) = Im(x^H y) = -r2(x).r1(y)
+//   ||r1(x)-r1(y)|| = ||r2(x)-r2(y)|| = ||x-y||,
+//   ||r1(x)-r2(y)|| = ||x+iy||,  ||r2(x)-r1(y)|| = ||x-iy||.
+// Distances use explicit differences (kernels.py:187-191), never the
+// ||a||^2+||b||^2-2ab expansion, so near-coincident pilots keep full
+// precision.  Every sum is formed in an order that makes the matrix exactly
+// symmetric (thread (q,p) reproduces thread (p,q)'s transpose bit for bit).
+#include "kapsm_common.cuh"
+
+namespace kapsm {
+
+constexpr int GRAM_TILE = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
+    pilot_gram_kernel(const T* __restrict__ rx, long long rx_stride, int n_train, int M,
+                      T w_l, T w_g, T inv2s, T* __restrict__ gram, long long ld,
+                      long long gram_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xa = reinterpret_cast<T*>(smem_raw);        // [GRAM_TILE][2M]
+  T* xb = xa + GRAM_TILE * 2 * M;                // [GRAM_TILE][2M]
+  const int f = blockIdx.z;
+  const T* X = rx + (long long)f * rx_stride;
+  const int p0 = blockIdx.y * GRAM_TILE, q0 = blockIdx.x * GRAM_TILE;
+  const int tid = threadIdx.y * GRAM_TILE + threadIdx.x;
+  const int row_elems = 2 * M;
+  for (int e = tid; e < GRAM_TILE * row_elems; e += GRAM_TILE * GRAM_TILE) {
+    int r = e / row_elems, c = e - r * row_elems;
+    xa[e] = (p0 + r < n_train) ? X[(long long)(p0 + r) * row_elems + c] : T(0);
+    xb[e] = (q0 + r < n_train) ? X[(long long)(q0 + r) * row_elems + c] : T(0);
+  }
+  __syncthreads();
+  const int p = p0 + threadIdx.y, q = q0 + threadIdx.x;
+  if (p >= n_train || q >= n_train) return;
+  const T* x = xa + threadIdx.y * row_elems;
+  const T* y = xb + threadIdx.x * row_elems;
+  T s_rr = 0, s_ii = 0, s_ri = 0, s_ir = 0, d_a = 0, d_b = 0, d_c = 0;
+  for (int k = 0; k < M; ++k) {
+    const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+    s_rr = fma(xr, yr, s_rr);
+    s_ii = fma(xi, yi, s_ii);
+    s_ri = fma(xr, yi, s_ri);
+    s_ir = fma(xi, yr, s_ir);
+    T a0, a1;
+    if constexpr (sizeof(T) == 4) {
+      a0 = __fsub_rn(xr, yr); a1 = __fsub_rn(xi, yi);
+      d_a = __fadd_rn(d_a, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+      a0 = __fsub_rn(xr, yi); a1 = __fadd_rn(xi, yr);                 // x + i y
+      d_b = __fadd_rn(d_b, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+      a0 = __fadd_rn(xr, yi); a1 = __fsub_rn(xi, yr);                 // x - i y
+      d_c = __fadd_rn(d_c, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+    } else {
+      a0 = __dsub_rn(xr, yr); a1 = __dsub_rn(xi, yi);
+      d_a = __dadd_rn(d_a, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+      a0 = __dsub_rn(xr, yi); a1 = __dadd_rn(xi, yr);
+      d_b = __dadd_rn(d_b, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+      a0 = __dadd_rn(xr, yi); a1 = __dsub_rn(xi, yr);
+      d_c = __dadd_rn(d_c, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+    }
+  }
+  const T lin_re = s_rr + s_ii;          // Re(x^H y)
+  const T lin_12 = s_ri - s_ir;          // r1(x).r2(y)
+  const T lin_21 = s_ir - s_ri;          // r2(x).r1(y)
+  T g_a = 0, g_b = 0, g_c = 0;
+  if (w_g != T(0)) {
+    g_a = exp_acc(-d_a * inv2s);
+    g_b = exp_acc(-d_b * inv2s);
+    g_c = exp_acc(-d_c * inv2s);
+  }
+  const T k11 = w_l * lin_re + w_g * g_a;
+  const T k12 = w_l * lin_12 + w_g * g_b;
+  const T k21 = w_l * lin_21 + w_g * g_c;
+  using V2 = typename Vec2<T>::type;
+  T* G = gram + (long long)f * gram_stride;
+  V2 top, bot;
+  top.x = k11; top.y = k12;
+  bot.x = k21; bot.y = k11;
+  *reinterpret_cast<V2*>(G + (long long)(2 * p) * ld + 2 * q) = top;
+  *reinterpret_cast<V2*>(G + (long long)(2 * p + 1) * ld + 2 * q) = bot;
+}
+
+template <typename T>
+int pilot_gram(const T* rx, long long rx_stride, int F, int n_train, int M,
+               kapsm_kernel_params p, T* gram, long long ld, long long gram_stride,
+               cudaStream_t s) {
+  if (F < 0 || n_train < 0 || M < 1 || ld < 2LL * n_train || (ld & 1) || !rx || !gram)
+    return KAPSM_ERR_INVALID;
+  if (F == 0 || n_train == 0) return KAPSM_OK;
+  const int nt = (n_train + GRAM_TILE - 1) / GRAM_TILE;
+  dim3 grid(nt, nt, F), block(GRAM_TILE, GRAM_TILE);
+  size_t smem = 2 * GRAM_TILE * 2 * (size_t)M * sizeof(T);
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(pilot_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return KAPSM_ERR_CUDA;
+  }
+  pilot_gram_kernel<T><<<grid, block, smem, s>>>(rx, rx_stride, n_train, M, (T)p.w_l, (T)p.w_g,
+                                                 (T)(1.0 / (2.0 * p.sigma_sq)), gram, ld,
+                                                 gram_stride);
+  return status_from(cudaGetLastError());
+}
+
+
+// Generic variant for arbitrary realified sample rows (ApsmTrainer.observe on
+// any real stream, apsm.py:304): samples F x (N x D), row-major.
+template <typename T>
+__global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
+    sample_gram_kernel(const T* __restrict__ S, long long s_stride, int N, int D, T w_l, T w_g,
+                       T inv2s, T* __restrict__ gram, long long ld, long long gram_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sa = reinterpret_cast<T*>(smem_raw);   // [GRAM_TILE][D]
+  T* sb = sa + GRAM_TILE * D;
+  const int f = blockIdx.z;
+  const T* Sf = S + (long long)f * s_stride;
+  const int i0 = blockIdx.y * GRAM_TILE, j0 = blockIdx.x * GRAM_TILE;
+  const int tid = threadIdx.y * GRAM_TILE + threadIdx.x;
+  for (int e = tid; e < GRAM_TILE * D; e += GRAM_TILE * GRAM_TILE) {
+    int r = e / D, c = e - r * D;
+    sa[e] = (i0 + r < N) ? Sf[(long long)(i0 + r) * D + c] : T(0);
+    sb[e] = (j0 + r < N) ? Sf[(long long)(j0 + r) * D + c] : T(0);
+  }
+  __syncthreads();
+  const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
+  if (i >= N || j >= N) return;
+  const T* a = sa + threadIdx.y * D;
+  const T* b = sb + threadIdx.x * D;
+  T dot = T(0), d2 = T(0);
+  for (int k = 0; k < D; ++k) {
+    dot = fma(a[k], b[k], dot);
+    const T e = a[k] - b[k];
+    d2 = fma(e, e, d2);
+  }
+  T g = T(0);
+  if (w_g != T(0)) g = exp_acc(-d2 * inv2s);
+  gram[(long long)f * gram_stride + (long long)i * ld + j] = w_l * dot + w_g * g;
+}
+
+template <typename T>
+int sample_gram(const T* S, long long s_stride, int F, int N, int D, kapsm_kernel_params p,
+                T* gram, long long ld, long long gram_stride, cudaStream_t s) {
+  if (F < 0 || N < 0 || D < 1 || ld < N || !S || !gram) return KAPSM_ERR_INVALID;
+  if (F == 0 || N == 0) return KAPSM_OK;
+  const int nt = (N + GRAM_TILE - 1) / GRAM_TILE;
+  dim3 grid(nt, nt, F), block(GRAM_TILE, GRAM_TILE);
+  size_t smem = 2 * GRAM_TILE * (size_t)D * sizeof(T);
+  if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(sample_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  sample_gram_kernel<T><<<grid, block, smem, s>>>(S, s_stride, N, D, (T)p.w_l, (T)p.w_g,
+                                                  (T)(1.0 / (2.0 * p.sigma_sq)), gram, ld,
+                                                  gram_stride);
+  return status_from(cudaGetLastError());
+}
+
+}  // namespace kapsm
+
+extern "C" int kapsm_sample_gram_f32(const float* S, long long s_stride, int F, int N, int D,
+                                     kapsm_kernel_params p, float* gram, long long ld,
+                                     long long gram_stride, void* stream) {
+  return kapsm::sample_gram<float>(S, s_stride, F, N, D, p, gram, ld, gram_stride,
+                                   (cudaStream_t)stream);
+}
+extern "C" int kapsm_sample_gram_f64(const double* S, long long s_stride, int F, int N, int D,
+                                     kapsm_kernel_params p, double* gram, long long ld,
+                                     long long gram_stride, void* stream) {
+  return kapsm::sample_gram<double>(S, s_stride, F, N, D, p, gram, ld, gram_stride,
+                                    (cudaStream_t)stream);
+}
+
+extern "C" int kapsm_pilot_gram_f32(const float* rx, long long rx_stride, int F, int n_train,
+                                    int M, kapsm_kernel_params p, float* gram, long long ld,
+                                    long long gram_stride, void* stream) {
+  return kapsm::pilot_gram<float>(rx, rx_stride, F, n_train, M, p, gram, ld, gram_stride,
+                                  (cudaStream_t)stream);
+}
+extern "C" int kapsm_pilot_gram_f64(const double* rx, long long rx_stride, int F, int n_train,
+                                    int M, kapsm_kernel_params p, double* gram, long long ld,
+                                    long long gram_stride, void* stream) {
+  return kapsm::pilot_gram<double>(rx, rx_stride, F, n_train, M, p, gram, ld, gram_stride,
+                                   (cudaStream_t)stream);
+}

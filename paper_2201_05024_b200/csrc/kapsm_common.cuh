@@ -1,0 +1,94 @@
+// Shared device helpers for the sm_100a APSM kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/kapsm_b200.h"
+
+#define KAPSM_DEV __device__ __forceinline__
+
+namespace kapsm {
+
+template <typename T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+KAPSM_DEV float exp_fast(float x) {  // x <= 0; MUFU.EX2 path
+  return exp2f(x * 1.4426950408889634f);
+}
+KAPSM_DEV double exp_fast(double x) { return exp(x); }
+KAPSM_DEV float exp_acc(float x) { return expf(x); }
+KAPSM_DEV double exp_acc(double x) { return exp(x); }
+
+template <typename T>
+KAPSM_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+KAPSM_DEV unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+KAPSM_DEV int ld_volatile(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "l"(__cvta_generic_to_shared(p)));
+  return v;
+}
+KAPSM_DEV void st_volatile(int* p, int v) {
+  asm volatile("st.volatile.shared.s32 [%0], %1;" ::"l"(__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+
+// Tagged value slots: (value, tag) published with ONE shared-memory store so a
+// reader that sees the tag also sees the value (no reader-side fence).
+template <typename T> struct Tagged;
+template <> struct Tagged<float> {
+  using slot_t = unsigned long long;
+  static KAPSM_DEV void store(slot_t* p, float v, int tag) {
+    unsigned long long w = ((unsigned long long)(unsigned)tag << 32) | __float_as_uint(v);
+    asm volatile("st.volatile.shared.u64 [%0], %1;" ::"l"(__cvta_generic_to_shared(p)), "l"(w)
+                 : "memory");
+  }
+  static KAPSM_DEV bool load(const slot_t* p, int tag, float& v) {
+    unsigned long long w;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "l"(__cvta_generic_to_shared(p)));
+    v = __uint_as_float((unsigned)(w & 0xffffffffu));
+    return (int)(w >> 32) == tag;
+  }
+};
+template <> struct Tagged<double> {
+  struct __align__(16) slot_t { unsigned long long v, t; };
+  static KAPSM_DEV void store(slot_t* p, double v, int tag) {
+    asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"l"(__cvta_generic_to_shared(p)),
+                 "l"(__double_as_longlong(v)), "l"((unsigned long long)(unsigned)tag)
+                 : "memory");
+  }
+  static KAPSM_DEV bool load(const slot_t* p, int tag, double& v) {
+    unsigned long long a, b;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(a), "=l"(b)
+                 : "l"(__cvta_generic_to_shared(p)));
+    v = __longlong_as_double((long long)a);
+    return (int)b == tag;
+  }
+};
+
+// cp.async of one scalar (4 or 8 bytes) global -> shared.
+template <typename T>
+KAPSM_DEV void cp_async_scalar(T* smem_dst, const T* gmem_src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+KAPSM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+KAPSM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+inline int status_from(cudaError_t e) { return e == cudaSuccess ? KAPSM_OK : KAPSM_ERR_CUDA; }
+
+}  // namespace kapsm

@@ -1,0 +1,60 @@
+// One-call frame pipeline: K1 (pilot Gram) -> K2 (persistent trainer, all K
+// users of all F frames) -> K3 (fused detection + demap + error count), all on
+// one stream, no host synchronisation, no allocation -- the unit that the
+// host captures into a CUDA graph.  Composition of run_trial
+// (noma.py:249-281) for every target user of each frame.
+#include "kapsm_common.cuh"
+
+template <typename T> struct Fns;
+template <> struct Fns<float> {
+  static constexpr auto gram = kapsm_pilot_gram_f32;
+  static constexpr auto train = kapsm_train_f32;
+  static constexpr auto detect = kapsm_detect_frames_f32;
+};
+template <> struct Fns<double> {
+  static constexpr auto gram = kapsm_pilot_gram_f64;
+  static constexpr auto train = kapsm_train_f64;
+  static constexpr auto detect = kapsm_detect_frames_f64;
+};
+
+template <typename T>
+static int run_frames(const T* rx, long long rx_stride, const T* pilots,
+                      const unsigned char* tx_labels, int F, int K, int n_train, int n_data, int M,
+                      int window, double eps, kapsm_kernel_params p, const T* qtab,
+                      const T* points, int n_points, int bps, T* gram_ws, long long ld, T* coeff,
+                      int* first_step, T* theta, int* n_active, int* status, T* est,
+                      unsigned char* labels, unsigned long long* bit_err,
+                      unsigned long long* sym_err, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (F < 0 || K < 1 || n_train < 1 || n_data < 0 || M < 1) return KAPSM_ERR_INVALID;
+  if (F == 0) return KAPSM_OK;
+  const int Np = 2 * n_train;
+  if (bit_err && cudaMemsetAsync(bit_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  if (sym_err && cudaMemsetAsync(sym_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  const long long gstride = (long long)Np * ld;
+  int r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream);
+  if (r) return r;
+  r = Fns<T>::train(gram_ws, ld, gstride, rx, rx_stride, nullptr, 0, 2 * M, pilots, F, K, Np,
+                    window, eps, p, qtab, nullptr, nullptr, coeff, first_step, theta, n_active,
+                    status, stream);
+  if (r) return r;
+  return Fns<T>::detect(rx, rx_stride, F, K, n_train, n_data, M, coeff, theta, p, points,
+                        n_points, bps, tx_labels, est, labels, bit_err, sym_err, stream);
+}
+
+#define KAPSM_RUN_ENTRY(NAME, T)                                                               \
+  extern "C" int NAME(const T* rx, long long rx_stride, const T* pilots,                       \
+                      const unsigned char* tx_labels, int F, int K, int n_train, int n_data,   \
+                      int M, int window, double eps, kapsm_kernel_params p, const T* qtab,     \
+                      const T* points, int n_points, int bps, T* gram_ws, long long ld,        \
+                      T* coeff, int* first_step, T* theta, int* n_active, int* status, T* est, \
+                      unsigned char* labels, unsigned long long* bit_err,                      \
+                      unsigned long long* sym_err, void* stream) {                             \
+    return run_frames<T>(rx, rx_stride, pilots, tx_labels, F, K, n_train, n_data, M, window,   \
+                         eps, p, qtab, points, n_points, bps, gram_ws, ld, coeff, first_step,  \
+                         theta, n_active, status, est, labels, bit_err, sym_err, stream);      \
+  }
+KAPSM_RUN_ENTRY(kapsm_run_frames_f32, float)
+KAPSM_RUN_ENTRY(kapsm_run_frames_f64, double)

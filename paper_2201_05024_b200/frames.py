@@ -1,0 +1,174 @@
+"""Frame-batched device pipeline: F frames x K users, train on each frame's
+pilots, detect its payload, decide and count errors -- all on the GPU.
+
+This is the throughput/latency entry point (the reference composes the same
+work per user in ``run_trial``, noma.py:249-281).  Buffers are allocated once
+per shape; ``launch`` issues the one-call C pipeline (``kapsm_run_frames_*``:
+K1 Gram -> K2 persistent trainer -> K3 fused detect/demap/count) on the current
+stream; ``capture`` records it into a CUDA graph replayed by ``replay``.
+
+Layout (HBM): rx (F, T, M, 2) interleaved complex, pilots (F, K, n_train, 2),
+tx labels (F, K, n_data) uint8; Gram workspace (F, Np, ld).
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .apsm import ApsmConfig, qtab_device
+from .noma import get_constellation, points_device
+
+__all__ = ["FramePipeline", "host_frames"]
+
+
+def _ld(n: int) -> int:
+    return max(32, (n + 31) // 32 * 32)
+
+
+class FramePipeline:
+    def __init__(self, F: int, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
+                 cfg: Optional[ApsmConfig] = None, precision: str = "f32",
+                 store_est: bool = True, device=None):
+        if precision not in dv.DTYPES:
+            raise ValueError(f"precision must be 'f64' or 'f32', got {precision!r}")
+        self.cfg = cfg or ApsmConfig()
+        self.F, self.K, self.M, self.n_train, self.n_data = F, K, M, n_train, n_data
+        self.T = n_train + n_data
+        self.Np = 2 * n_train
+        self.scheme = scheme
+        self.prec = precision
+        con = get_constellation(scheme)
+        self.n_points, self.bps = con.points.size, con.bits_per_symbol
+        lib = _lib.load()
+        if self.cfg.window > lib.kapsm_max_window() or self.Np > lib.kapsm_max_samples():
+            raise NotImplementedError(
+                f"window {self.cfg.window} / {self.Np} pilot samples exceed the trainer limits "
+                f"(window <= {lib.kapsm_max_window()}, samples <= {lib.kapsm_max_samples()})")
+        dev = dv.device() if device is None else device
+        tdt = dv.DTYPES[precision][0]
+        z = lambda *s, dt=tdt: torch.zeros(s, dtype=dt, device=dev)
+        self.rx = z(F, self.T, M, 2)
+        self.pilots = z(F, K, n_train, 2)
+        self.tx = z(F, K, n_data, dt=torch.uint8)
+        self.ld = _ld(self.Np)
+        self.gram = z(F, self.Np, self.ld)
+        self.coeff = z(F, K, self.Np)
+        self.first_step = z(F, K, self.Np, dt=torch.int32)
+        self.theta = z(F, K, 2 * M)
+        self.n_active = z(F, K, dt=torch.int32)
+        self.status = z(F, K, dt=torch.int32)
+        self.est = z(F, K, n_data, 2) if store_est else None
+        self.labels = z(F, K, n_data, dt=torch.uint8)
+        self.bit_err = z(F, K, dt=torch.int64)
+        self.sym_err = z(F, K, dt=torch.int64)
+        self.qtab = qtab_device(self.cfg.window, precision)
+        self.points = points_device(scheme, precision)
+        self.graph = None
+        self._fn = dv.fn("kapsm_run_frames", precision)
+
+    # -- inputs -------------------------------------------------------------
+    def load(self, rx, pilots, tx_labels, non_blocking: bool = False):
+        """Copy one batch (host complex arrays or device tensors) into the static buffers."""
+        def put(dst, src, cplx):
+            if isinstance(src, torch.Tensor):
+                dst.copy_(src, non_blocking=non_blocking)
+            else:
+                a = np.asarray(src)
+                if cplx:
+                    a = np.stack([a.real, a.imag], axis=-1)
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(a)).to(dst.dtype),
+                          non_blocking=non_blocking)
+        put(self.rx, rx, True)
+        put(self.pilots, pilots, True)
+        put(self.tx, tx_labels, False)
+
+    # -- compute ------------------------------------------------------------
+    def _args(self):
+        c = self.cfg
+        return (dv.ptr(self.rx), self.T * self.M * 2, dv.ptr(self.pilots), dv.ptr(self.tx),
+                self.F, self.K, self.n_train, self.n_data, self.M, c.window, float(c.epsilon),
+                _lib.params(c.params), dv.ptr(self.qtab), dv.ptr(self.points), self.n_points,
+                self.bps, dv.ptr(self.gram), self.ld, dv.ptr(self.coeff),
+                dv.ptr(self.first_step), dv.ptr(self.theta), dv.ptr(self.n_active),
+                dv.ptr(self.status), dv.ptr(self.est), dv.ptr(self.labels),
+                dv.ptr(self.bit_err), dv.ptr(self.sym_err))
+
+    def launch(self, time_detect: bool = False):
+        """Enqueue the whole pipeline on the current stream.  With time_detect,
+        run the stages separately and return the detection kernel time in us."""
+        if not time_detect:
+            _lib.check(self._fn(*self._args(), dv.stream()), "run_frames")
+            return None
+        lib = _lib.load()
+        c = self.cfg
+        p = _lib.params(c.params)
+        st = dv.stream()
+        pre = self.prec
+        self.bit_err.zero_()
+        self.sym_err.zero_()
+        gstride = self.Np * self.ld
+        _lib.check(dv.fn("kapsm_pilot_gram", pre)(dv.ptr(self.rx), self.T * self.M * 2, self.F,
+                                                  self.n_train, self.M, p, dv.ptr(self.gram),
+                                                  self.ld, gstride, st), "pilot_gram")
+        _lib.check(dv.fn("kapsm_train", pre)(
+            dv.ptr(self.gram), self.ld, gstride, dv.ptr(self.rx), self.T * self.M * 2,
+            dv.ptr(None), 0, 2 * self.M, dv.ptr(self.pilots), self.F, self.K, self.Np, c.window,
+            float(c.epsilon), p, dv.ptr(self.qtab), dv.ptr(None), dv.ptr(None),
+            dv.ptr(self.coeff), dv.ptr(self.first_step), dv.ptr(self.theta),
+            dv.ptr(self.n_active), dv.ptr(self.status), st), "train")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(dv.fn("kapsm_detect_frames", pre)(
+            dv.ptr(self.rx), self.T * self.M * 2, self.F, self.K, self.n_train, self.n_data,
+            self.M, dv.ptr(self.coeff), dv.ptr(self.theta), p, dv.ptr(self.points),
+            self.n_points, self.bps, dv.ptr(self.tx), dv.ptr(self.est), dv.ptr(self.labels),
+            dv.ptr(self.bit_err), dv.ptr(self.sym_err), st), "detect_frames")
+        e1.record()
+        e1.synchronize()
+        del lib
+        return e0.elapsed_time(e1) * 1e3
+
+    def capture(self):
+        """Record one launch into a CUDA graph (static shapes and buffers)."""
+        self.launch()                       # warm-up: sets kernel attributes outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch()
+        self.graph = g
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    # -- outputs ------------------------------------------------------------
+    def results(self, est: bool = True) -> dict:
+        out = dict(labels=self.labels.cpu().numpy(), bit_err=self.bit_err.cpu().numpy(),
+                   sym_err=self.sym_err.cpu().numpy(), n_active=self.n_active.cpu().numpy(),
+                   status=self.status.cpu().numpy(), theta=self.theta.cpu().numpy(),
+                   coeff=self.coeff.cpu().numpy(), first_step=self.first_step.cpu().numpy())
+        if est and self.est is not None:
+            e = self.est.cpu().numpy().astype(np.float64)
+            out["est"] = e[..., 0] + 1j * e[..., 1]
+        return out
+
+
+def host_frames(seeds, K, M, n_train, n_data, scheme="QPSK", snr_db=20.0):
+    """Seeded host frames in the reference's RNG order -> (rx, pilots, tx_labels, bits)."""
+    from .noma import seeded_frame, symbol_labels
+    rxs, pils, txs, bits = [], [], [], []
+    for s in seeds:
+        fr = seeded_frame(int(s), K, M, n_train, n_data, scheme, snr_db)
+        k = fr["bps"]
+        rxs.append(fr["rx"])
+        pils.append(fr["symbols"][:, :n_train])
+        txs.append(symbol_labels(fr["bits"][:, n_train * k:], k))
+        bits.append(fr["bits"])
+    return np.stack(rxs), np.stack(pils), np.stack(txs), np.stack(bits)

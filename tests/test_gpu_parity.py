@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle and the
+reference's golden vectors.  Bars (north star): hard decisions and error
+counts exact; soft estimates within 1e-4 relative (max-norm) in FP32; the
+FP64 kernels within 1e-9 of the reference (its own engine tolerance,
+test_engine.py:49-55)."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_2201_05024_b200 as K
+from oracle import kapsm_oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SMALL = sorted(glob.glob(os.path.join(GOLDEN, "small_*.npz")))
+P = K.KernelParams(0.5, 0.5, 0.05)
+
+
+def maxrel(a, b):
+    d = np.max(np.abs(b))
+    return float(np.max(np.abs(a - b)) / d) if d else float(np.max(np.abs(a - b)))
+
+
+def gram_np(R, p=P):
+    d2 = ((R[:, None, :] - R[None, :, :]) ** 2).sum(-1)
+    return p.w_l * (R @ R.T) + p.w_g * np.exp(-d2 / (2 * p.sigma_sq))
+
+
+# --------------------------------------------------------------------------- K1
+@pytest.mark.parametrize("prec,tol", [("f32", 2e-6), ("f64", 1e-13)])
+def test_pilot_gram(prec, tol):
+    import torch
+    from paper_2201_05024_b200 import _device as dv, _lib
+    rng = np.random.default_rng(0)
+    for (T, M, scale) in ((37, 3, 0.3), (50, 16, 1.0), (20, 5, 0.05)):
+        x = scale * (rng.standard_normal((T, M)) + 1j * rng.standard_normal((T, M)))
+        x[7] = x[3] + 1e-3          # near-duplicate pilots: live Gaussian terms
+        N, ld = 2 * T, 2 * T + 32
+        xd = dv.complex_to_dev(x, prec)
+        g = dv.empty((N, ld), prec)
+        _lib.check(dv.fn("kapsm_pilot_gram", prec)(dv.ptr(xd), 2 * T * M, 1, T, M,
+                                                    _lib.params(P), dv.ptr(g), ld, N * ld,
+                                                    dv.stream()), "gram")
+        G = g.cpu().numpy()[:, :N].astype(np.float64)
+        assert np.array_equal(G, G.T)                       # exactly symmetric
+        ref = gram_np(O.realify(x))
+        assert maxrel(G, ref) < tol
+
+
+# --------------------------------------------------------------------------- K2
+def _frame(g):
+    return O.make_frame(int(g["seed"]), int(g["K"]), int(g["M"]), int(g["n_train"]),
+                        int(g["n_data"]), str(g["scheme"]))
+
+
+@pytest.mark.parametrize("path", SMALL, ids=[os.path.basename(p) for p in SMALL])
+def test_train_f64_matches_reference(path):
+    g = np.load(path)
+    fr = _frame(g)
+    nt = int(g["n_train"])
+    R = O.realify(fr["rx"][:nt])
+    for u in g["users"]:
+        f = K.train(None, zip(fr["rx"][:nt], fr["symbols"][u, :nt]), K.ApsmConfig(),
+                    precision="f64")
+        assert f.n_atoms == int(g[f"u{u}_n_atoms"])
+        assert np.array_equal(f.atoms, R[g[f"u{u}_atom_idx"]])       # same atoms, same slot order
+        np.testing.assert_allclose(f.theta, g[f"u{u}_theta"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(f.coeffs, g[f"u{u}_coeffs"], rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("path", SMALL, ids=[os.path.basename(p) for p in SMALL])
+def test_train_f32_close_to_reference(path):
+    g = np.load(path)
+    fr = _frame(g)
+    nt = int(g["n_train"])
+    for u in g["users"]:
+        f = K.train(None, zip(fr["rx"][:nt], fr["symbols"][u, :nt]), K.ApsmConfig(),
+                    precision="f32")
+        assert f.n_atoms == int(g[f"u{u}_n_atoms"])
+        assert maxrel(f.theta, g[f"u{u}_theta"]) < 1e-4
+
+
+def test_trainer_generic_stream_and_warm_start():
+    """ApsmTrainer on an arbitrary real stream (apsm.py:304) with a warm start."""
+    rng = np.random.default_rng(12)
+    cfg = K.ApsmConfig(window=6, epsilon=0.05, params=P)
+    R = rng.standard_normal((120, 4)) * 0.3
+    B = rng.standard_normal(120)
+    tr = K.ApsmTrainer(4, cfg)
+    for r, b in zip(R, B):
+        tr.observe(r, b)
+    f = tr.state()
+    ref = O.train_user(R, B, W=6, eps=0.05)
+    assert f.n_atoms == ref["n_atoms"]
+    np.testing.assert_allclose(f.theta, ref["theta"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(f.coeffs, ref["coeffs"], rtol=1e-8, atol=1e-12)
+    # warm start: prefix preserved (test_apsm.py:305-311)
+    f0 = K.from_expansion([0.7], [[0.1, 0.2, 0.0, 0.0]], P)
+    t2 = K.ApsmTrainer(4, K.ApsmConfig(params=P), f0=f0)
+    assert t2.state().n_atoms == 1
+    t2.observe(R[0], 3.0)
+    s = t2.state()
+    assert np.array_equal(s.atoms[0], f0.atoms[0]) and s.coeffs[0] == 0.7
+    # the warm-started update lands on the eps boundary (single projection)
+    y = K.evaluate(s, R[0], P)
+    assert abs(abs(y - 3.0) - 0.01) < 1e-9
+
+
+def test_train_literal_path_equivalence():
+    """Coalesced trainer == literal apsm_step path (test_apsm.py:220-243)."""
+    rng = np.random.default_rng(7)
+    cfg = K.ApsmConfig(window=5, epsilon=0.02, params=P)
+    stream = [(rng.standard_normal(3) * 0.4 + 1j * rng.standard_normal(3) * 0.4,
+               complex(rng.standard_normal(), rng.standard_normal())) for _ in range(40)]
+    f_fast = K.train(None, stream, cfg)
+    f = K.zero_filter(6)
+    hist = []
+    for r, b in stream:
+        for s in K.complex_to_real_pair(r, b):
+            hist.append(s)
+            n = len(hist) - 1
+            f = K.apsm_step(f, [hist[i] for i in K.window_indices(n, cfg.window)], cfg)
+    assert f.n_atoms >= f_fast.n_atoms
+    np.testing.assert_allclose(f_fast.theta, f.theta, rtol=1e-9, atol=1e-12)
+    u = rng.standard_normal((30, 6)) * 0.5
+    a = K.batch_evaluate(f_fast, u, P, K.EngineConfig())
+    b = K.batch_evaluate(f, u, P, K.EngineConfig())
+    np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-12)
+
+
+def test_train_errors():
+    rng = np.random.default_rng(11)
+    cfg = K.ApsmConfig(window=4, epsilon=0.01, params=P, max_atoms=5)
+    stream = [(rng.standard_normal(2) + 1j * rng.standard_normal(2), complex(3.0, 3.0))
+              for _ in range(50)]
+    with pytest.raises(K.DictionaryCapacityError):
+        K.train(None, stream, cfg)
+    lin = K.KernelParams(1.0, 0.0, 0.05)
+    with pytest.raises(ValueError):
+        K.train(None, [(np.zeros(2, complex), 1 + 1j)], K.ApsmConfig(params=lin))
+    with pytest.raises(ValueError):
+        K.train(None, [], K.ApsmConfig())
+    f = K.train(None, [(rng.standard_normal(2) + 1j * rng.standard_normal(2), complex(1, -1))
+                       for _ in range(30)], K.ApsmConfig(window=4, epsilon=0.02, params=lin))
+    assert f.n_atoms == 0
+
+
+# --------------------------------------------------------------------------- K3 / pipeline
+@pytest.mark.parametrize("path", SMALL, ids=[os.path.basename(p) for p in SMALL])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_pipeline_small_frames(path, prec):
+    g = np.load(path)
+    Kn, M, nt, nd, sch = int(g["K"]), int(g["M"]), int(g["n_train"]), int(g["n_data"]), str(g["scheme"])
+    rx, pil, tx, bits = K.host_frames([int(g["seed"])], Kn, M, nt, nd, sch)
+    pipe = K.FramePipeline(1, Kn, M, nt, nd, sch, precision=prec)
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    r = pipe.results()
+    tol = 1e-4 if prec == "f32" else 1e-9
+    kbits = K.get_constellation(sch).bits_per_symbol
+    for u in range(Kn):
+        est = g[f"u{u}_est"]
+        assert maxrel(r["est"][0, u], est) < tol, (u, maxrel(r["est"][0, u], est))
+        assert int(r["bit_err"][0, u]) == int(g[f"u{u}_bit_err"])
+        assert int(r["n_active"][0, u]) == int(g[f"u{u}_n_atoms"])
+        ref_idx = O.demap_indices(est, sch)
+        assert np.array_equal(r["labels"][0, u], ref_idx)
+        assert int(r["sym_err"][0, u]) == int(np.sum(ref_idx != tx[0, u]))
+    assert np.all(r["status"] == 0)
+
+
+def test_pipeline_c1_paper_frame():
+    """C1 (K=6, M=16, QPSK, 685/3840) FP32: estimates within 1e-4 of the
+    reference (users 0, 1 golden; all users vs the oracle), decisions exact."""
+    g = np.load(os.path.join(GOLDEN, "c1_s0_users01.npz"))
+    rx, pil, tx, bits = K.host_frames([0], 6, 16, 685, 3840, "QPSK")
+    pipe = K.FramePipeline(1, 6, 16, 685, 3840, "QPSK", precision="f32")
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    r = pipe.results()
+    for u in (0, 1):
+        assert maxrel(r["est"][0, u], g[f"u{u}_est"]) < 1e-4
+        assert int(r["bit_err"][0, u]) == int(g[f"u{u}_bit_err"])
+        assert int(r["n_active"][0, u]) == int(g[f"u{u}_n_atoms"])
+    fr = O.make_frame(0, 6, 16, 685, 3840, "QPSK")
+    for res in O.run_frame(fr, 685, "QPSK", users=[2, 3, 4, 5]):
+        u = res["user"]
+        assert maxrel(r["est"][0, u], res["est"]) < 1e-4
+        assert np.array_equal(r["labels"][0, u], res["rx_idx"])
+        assert int(r["bit_err"][0, u]) == res["bit_err"]
+
+
+def test_graph_replay_matches_eager():
+    rx, pil, tx, _ = K.host_frames([3, 4], 6, 16, 100, 160, "QPSK")
+    pipe = K.FramePipeline(2, 6, 16, 100, 160, "QPSK", precision="f32")
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    a = pipe.results()
+    pipe.capture()
+    for _ in range(3):
+        pipe.replay()
+    b = pipe.results()
+    assert np.array_equal(a["est"], b["est"])
+    assert np.array_equal(a["labels"], b["labels"])
+    assert np.array_equal(a["bit_err"], b["bit_err"])
+
+
+def test_multiframe_batch_equals_single():
+    """Frames in one batch are independent (weak-scaling shard property)."""
+    seeds = [5, 6, 7]
+    rx, pil, tx, _ = K.host_frames(seeds, 3, 4, 60, 80, "QPSK")
+    pipe = K.FramePipeline(3, 3, 4, 60, 80, "QPSK", precision="f32")
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    full = pipe.results()
+    for i in range(3):
+        p1 = K.FramePipeline(1, 3, 4, 60, 80, "QPSK", precision="f32")
+        p1.load(rx[i:i + 1], pil[i:i + 1], tx[i:i + 1])
+        p1.launch()
+        one = p1.results()
+        assert np.array_equal(one["est"][0], full["est"][i])
+        assert np.array_equal(one["bit_err"][0], full["bit_err"][i])
+
+
+# --------------------------------------------------------------------------- engine API
+def test_engine_golden_random_filter():
+    g = np.load(os.path.join(GOLDEN, "engine_random.npz"))
+    f = K.FilterState(g["theta"], g["atoms"], g["coeffs"])
+    out64 = K.batch_evaluate(f, g["inputs"], P, K.EngineConfig())
+    assert maxrel(out64, g["out_f64"]) <= 1e-9
+    out32 = K.batch_evaluate(f, g["inputs"], P, K.EngineConfig(precision="f32"))
+    assert maxrel(out32, g["out_f64"]) <= 1e-4
+    assert out32.dtype == np.float64
+
+
+@pytest.mark.parametrize("dim", [2, 5, 10, 33, 64])
+def test_batch_evaluate_random(dim):
+    rng = np.random.default_rng(dim)
+    f = K.FilterState(rng.standard_normal(dim), rng.standard_normal((123, dim)) * 0.3,
+                      rng.standard_normal(123))
+    u = rng.standard_normal((57, dim)) * 0.3
+    ref = O.evaluate_batch(f.theta, f.atoms, f.coeffs, u)
+    assert maxrel(K.batch_evaluate(f, u, P, K.EngineConfig()), ref) <= 1e-9
+    assert maxrel(K.batch_evaluate(f, u, P, K.EngineConfig(precision="f32")), ref) <= 1e-4
+
+
+def test_batch_detect_and_edges():
+    rng = np.random.default_rng(12)
+    f = K.FilterState(rng.standard_normal(10), rng.standard_normal((80, 10)) * 0.3,
+                      rng.standard_normal(80))
+    rx = rng.standard_normal((40, 5)) * 0.3 + 1j * rng.standard_normal((40, 5)) * 0.3
+    ref = O.detect_batch(f.theta, f.atoms, f.coeffs, rx)
+    out = K.batch_detect(f, rx, P, K.EngineConfig())
+    assert maxrel(out, ref) <= 1e-9
+    assert K.detect_symbol(f, rx[3], P) == pytest.approx(ref[3], rel=1e-9)
+    e = K.batch_detect(K.zero_filter(4), [], P, K.EngineConfig())
+    assert e.shape == (0,) and e.dtype == np.complex128
+    assert np.all(K.batch_evaluate(K.zero_filter(4), rng.standard_normal((9, 4)), P,
+                                   K.EngineConfig()) == 0.0)
+    with pytest.raises(ValueError):
+        K.batch_evaluate(K.zero_filter(4), np.zeros((3, 5)), P, K.EngineConfig())
+    lin = K.KernelParams(1.0, 0.0, 0.05)
+    u = rng.standard_normal((15, 10))
+    np.testing.assert_allclose(K.batch_evaluate(f, u, lin, K.EngineConfig()), u @ f.theta,
+                               rtol=1e-12)
+
+
+def test_demap_and_ber():
+    assert list(K.demodulate_hard(np.array([0j]), "QPSK")) == [0, 0]
+    assert list(K.demodulate_hard(np.array([0.9 + 0.8j]), "QPSK")) == [0, 0]
+    for scheme in K.SCHEMES:
+        con = K.get_constellation(scheme)
+        rng = np.random.default_rng(0)
+        bits = rng.integers(0, 2, 60 * con.bits_per_symbol)
+        assert np.array_equal(K.demodulate_hard(K.modulate(bits, scheme), scheme), bits)
+        est = rng.standard_normal(200) + 1j * rng.standard_normal(200)
+        assert np.array_equal(K.demodulate_hard(est, scheme), O.demodulate_hard(est, scheme))
+    assert K.ber([0, 1, 0], [1, 0, 1]) == 1.0
+    assert K.ber([0, 0, 1, 1], [0, 0, 0, 0]) == 0.5
+    with pytest.raises(ValueError):
+        K.ber([], [])
+
+
+def test_run_trial_reference_cases():
+    """noma.run_trial cases of the reference suite (test_noma.py:245-272)."""
+    rng = np.random.default_rng(40)
+    ch = K.draw_channel(1, 2, "uniform", 0.0, rng)
+    rep = K.run_trial(ch, K.FrameSpec(80, 200, "BPSK"), K.ApsmConfig(), K.EngineConfig(), 0, rng)
+    assert rep.ber == 0.0 and rep.trained_atoms > 0 and rep.detect_us > 0
+    ch = K.draw_channel(3, 4, "uniform", 0.05, np.random.default_rng(41))
+    reps = [K.run_trial(ch, K.FrameSpec(60, 150, "QPSK"), K.ApsmConfig(), K.EngineConfig(), 0,
+                        np.random.default_rng(7)) for _ in range(2)]
+    assert reps[0].ber == reps[1].ber and reps[0].trained_atoms == reps[1].trained_atoms
+    rng = np.random.default_rng(42)
+    ch = K.draw_channel(6, 16, "uniform", K.noise_var_for_snr(np.ones(6), 20.0), rng)
+    rep = K.run_trial(ch, K.FrameSpec(300, 600, "QPSK"), K.ApsmConfig(), K.EngineConfig(), 0, rng)
+    assert rep.ber < 1e-2
+    with pytest.raises(ValueError):
+        K.run_trial(K.draw_channel(2, 2, "uniform", 0.0, np.random.default_rng(43)),
+                    K.FrameSpec(10, 10), K.ApsmConfig(), K.EngineConfig(), 5,
+                    np.random.default_rng(0))
