@@ -24,7 +24,6 @@
 namespace kapsm {
 
 constexpr int DT_WARPS = 8;     // pilot split inside a CTA
-constexpr int DT_PC = 64;       // pilots per shared-memory chunk
 
 template <typename T> struct Thresh;
 template <> struct Thresh<float> {
@@ -40,10 +39,74 @@ template <> struct Thresh<double> {
   static constexpr bool refine = false;
 };
 
+template <typename T, int MT>
+KAPSM_DEV void cdot(const T* __restrict__ x, const T (&y)[2 * MT], T& cr, T& ci) {
+  // x^H y for MT complex entries; x is a 16-byte aligned shared-memory row
+  T r0 = T(0), r1 = T(0), i0 = T(0), i1 = T(0);
+  if constexpr (sizeof(T) == 4) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int q = 0; q < MT / 2; ++q) {
+      const float4 v = x4[q];            // (xr_k, xi_k, xr_k+1, xi_k+1)
+      r0 = fmaf(v.x, y[4 * q], r0);     r1 = fmaf(v.y, y[4 * q + 1], r1);
+      i0 = fmaf(v.x, y[4 * q + 1], i0); i1 = fmaf(v.y, y[4 * q], i1);
+      r0 = fmaf(v.z, y[4 * q + 2], r0); r1 = fmaf(v.w, y[4 * q + 3], r1);
+      i0 = fmaf(v.z, y[4 * q + 3], i0); i1 = fmaf(v.w, y[4 * q + 2], i1);
+    }
+  } else {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+      const double2 v = x2[k];
+      r0 = fma(v.x, y[2 * k], r0);     r1 = fma(v.y, y[2 * k + 1], r1);
+      i0 = fma(v.x, y[2 * k + 1], i0); i1 = fma(v.y, y[2 * k], i1);
+    }
+  }
+  cr = r0 + r1;
+  ci = i0 - i1;
+}
+
+// One (pilot, payload) pair: distances from the expansion, refine when a live
+// kernel meets large norms, exp, contract with every user's coefficients.
+template <typename T, int MT, int KT>
+KAPSM_DEV void pair_update(const T* x, T nx, const T* cp, const T (&y)[2 * MT], T ny, T cr, T ci,
+                           bool tvalid, T inv2s, T (&are)[KT], T (&aim)[KT]) {
+  const T s = nx + ny;
+  T da = s - T(2) * cr, db = s - T(2) * ci, dc = s + T(2) * ci;
+  const T dmin = fmin(da, fmin(db, dc));
+  const bool live = tvalid && dmin * inv2s < Thresh<T>::dead;
+  if (Thresh<T>::refine && live && dmin * inv2s < Thresh<T>::live && s * inv2s > Thresh<T>::bignorm) {
+    T ea = T(0), eb = T(0), ec = T(0);
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+      const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+      T a0 = xr - yr, a1 = xi - yi;
+      ea = fma(a0, a0, fma(a1, a1, ea));
+      a0 = xr - yi; a1 = xi + yr;
+      eb = fma(a0, a0, fma(a1, a1, eb));
+      a0 = xr + yi; a1 = xi - yr;
+      ec = fma(a0, a0, fma(a1, a1, ec));
+    }
+    da = ea; db = eb; dc = ec;
+  }
+  T ka = T(0), kb = T(0), kc = T(0);
+  if (live) {
+    ka = exp_fast(-fmax(da, T(0)) * inv2s);
+    kb = exp_fast(-fmax(db, T(0)) * inv2s);
+    kc = exp_fast(-fmax(dc, T(0)) * inv2s);
+  }
+#pragma unroll
+  for (int u = 0; u < KT; ++u) {
+    const T c1 = cp[2 * u], c2 = cp[2 * u + 1];
+    are[u] = fma(c1, ka, fma(c2, kc, are[u]));
+    aim[u] = fma(c1, kb, fma(c2, ka, aim[u]));
+  }
+}
+
 template <typename T, int MT, int KT>
 __global__ void __launch_bounds__(DT_WARPS * 32)
     detect_frames_kernel(const T* __restrict__ rx, long long rx_stride, int K, int n_train,
-                         int n_data, int M, const T* __restrict__ coeff,
+                         int n_data, int M, int PC, const T* __restrict__ coeff,
                          const T* __restrict__ theta, T w_g, T inv2s,
                          const T* __restrict__ points, int n_points, int bps,
                          const unsigned char* __restrict__ tx_labels, T* __restrict__ est_out,
@@ -51,12 +114,12 @@ __global__ void __launch_bounds__(DT_WARPS * 32)
                          unsigned long long* __restrict__ bit_err,
                          unsigned long long* __restrict__ sym_err) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // layout: pts[64][2], then chunk xs[DT_PC][2*MT], nxs[DT_PC], cs[DT_PC][2*KT];
-  // the epilogue's reduction buffer reuses the chunk area (never the points)
+  // layout: pts[64][2] | xs[PC][2*MT] | nxs[PC] | cs[PC][2*KT]; the epilogue's
+  // reduction buffer reuses the chunk area (never the points)
   T* pts = reinterpret_cast<T*>(smem);
   T* xs = pts + 128;
-  T* nxs = xs + DT_PC * 2 * MT;
-  T* cs = nxs + DT_PC;
+  T* nxs = xs + (size_t)PC * 2 * MT;
+  T* cs = nxs + PC;
   const int f = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 32 + lane;
@@ -82,83 +145,77 @@ __global__ void __launch_bounds__(DT_WARPS * 32)
 #pragma unroll
   for (int u = 0; u < KT; ++u) { are[u] = T(0); aim[u] = T(0); }
 
-  for (int c0 = 0; c0 < n_train; c0 += DT_PC) {
-    const int pc = min(DT_PC, n_train - c0);
+  for (int c0 = 0; c0 < n_train; c0 += PC) {
+    const int pc = min(PC, n_train - c0);
     __syncthreads();
-    for (int e = threadIdx.x; e < DT_PC * MT; e += blockDim.x) {
-      const int p = e / MT, k = e - p * MT;
-      T xr = T(0), xi = T(0);
-      if (p < pc && k < M) {
-        const T* xp = Xf + (long long)(c0 + p) * 2 * M + 2 * k;
-        xr = xp[0]; xi = xp[1];
+    // ---- stage the chunk: pilots (async copies), coefficients of all users ----
+    if (M == MT) {
+      const int nvec = pc * 2 * MT * (int)sizeof(T) / 16;
+      const char* src = reinterpret_cast<const char*>(Xf + (long long)c0 * 2 * M);
+      char* dst = reinterpret_cast<char*>(xs);
+      for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
+        unsigned d = (unsigned)__cvta_generic_to_shared(dst + 16 * e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 16 * (long long)e)
+                     : "memory");
       }
-      xs[p * 2 * MT + 2 * k] = xr;
-      xs[p * 2 * MT + 2 * k + 1] = xi;
+      cp_async_commit();
+    } else {
+      for (int e = threadIdx.x; e < pc * MT; e += blockDim.x) {
+        const int p = e / MT, k = e - p * MT;
+        T xr = T(0), xi = T(0);
+        if (k < M) {
+          const T* xp = Xf + (long long)(c0 + p) * 2 * M + 2 * k;
+          xr = xp[0]; xi = xp[1];
+        }
+        xs[p * 2 * MT + 2 * k] = xr;
+        xs[p * 2 * MT + 2 * k + 1] = xi;
+      }
     }
-    for (int e = threadIdx.x; e < DT_PC * KT; e += blockDim.x) {
-      const int p = e / KT, u = e - p * KT;
-      T c1 = T(0), c2 = T(0);
-      if (p < pc && u < K) {
-        const T* cu = coeff + ((long long)f * K + u) * Np + 2 * (c0 + p);
-        c1 = cu[0]; c2 = cu[1];
-      }
-      cs[p * 2 * KT + 2 * u] = c1;
-      cs[p * 2 * KT + 2 * u + 1] = c2;
+    using V2 = typename Vec2<T>::type;
+    for (int e = threadIdx.x; e < pc * KT; e += blockDim.x) {
+      const int u = e / pc, p = e - u * pc;          // consecutive threads -> consecutive pilots
+      V2 cc;
+      cc.x = T(0); cc.y = T(0);
+      if (u < K) cc = *reinterpret_cast<const V2*>(coeff + ((long long)f * K + u) * Np + 2 * (c0 + p));
+      *reinterpret_cast<V2*>(cs + p * 2 * KT + 2 * u) = cc;
+    }
+    if (M == MT) cp_async_wait<0>();
+    __syncthreads();
+    for (int p = threadIdx.x; p < pc; p += blockDim.x) {
+      T sacc = T(0);
+#pragma unroll 8
+      for (int k = 0; k < 2 * MT; ++k) sacc = fma(xs[p * 2 * MT + k], xs[p * 2 * MT + k], sacc);
+      nxs[p] = sacc;
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < DT_PC; p += blockDim.x) {
-      T s = T(0);
-#pragma unroll 4
-      for (int k = 0; k < 2 * MT; ++k) s = fma(xs[p * 2 * MT + k], xs[p * 2 * MT + k], s);
-      nxs[p] = s;
+    // ---- pairs: two pilots per iteration for ILP ----
+    int p = warp;
+    for (; p + DT_WARPS < pc; p += 2 * DT_WARPS) {
+      const int q = p + DT_WARPS;
+      const T* xp = xs + p * 2 * MT;
+      const T* xq = xs + q * 2 * MT;
+      T crp, cip, crq, ciq;
+      cdot<T, MT>(xp, y, crp, cip);
+      cdot<T, MT>(xq, y, crq, ciq);
+      const T np_ = nxs[p], nq_ = nxs[q];
+      const T dp = np_ + ny - T(2) * fmax(crp, fabs(cip));
+      const T dq = nq_ + ny - T(2) * fmax(crq, fabs(ciq));
+      const bool lp = tvalid && dp * inv2s < Thresh<T>::dead;
+      const bool lq = tvalid && dq * inv2s < Thresh<T>::dead;
+      if (__any_sync(0xffffffffu, lp))
+        pair_update<T, MT, KT>(xp, np_, cs + p * 2 * KT, y, ny, crp, cip, tvalid, inv2s, are, aim);
+      if (__any_sync(0xffffffffu, lq))
+        pair_update<T, MT, KT>(xq, nq_, cs + q * 2 * KT, y, ny, crq, ciq, tvalid, inv2s, are, aim);
     }
-    __syncthreads();
-    for (int p = warp; p < pc; p += DT_WARPS) {
-      const T* x = xs + p * 2 * MT;
-      T cr0 = T(0), cr1 = T(0), ci0 = T(0), ci1 = T(0);
-#pragma unroll
-      for (int k = 0; k < MT; ++k) {
-        const T xr = x[2 * k], xi = x[2 * k + 1];
-        cr0 = fma(xr, y[2 * k], cr0);
-        cr1 = fma(xi, y[2 * k + 1], cr1);
-        ci0 = fma(xr, y[2 * k + 1], ci0);
-        ci1 = fma(xi, y[2 * k], ci1);
-      }
-      const T cr = cr0 + cr1, ci = ci0 - ci1;
-      const T s = nxs[p] + ny;
-      T da = s - T(2) * cr, db = s - T(2) * ci, dc = s + T(2) * ci;
-      const T dmin = fmin(da, fmin(db, dc));
-      const bool live = tvalid && dmin * inv2s < Thresh<T>::dead;
-      if (__any_sync(0xffffffffu, live)) {
-        if (Thresh<T>::refine && live && dmin * inv2s < Thresh<T>::live &&
-            s * inv2s > Thresh<T>::bignorm) {
-          T ea = T(0), eb = T(0), ec = T(0);
-#pragma unroll
-          for (int k = 0; k < MT; ++k) {
-            const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
-            T a0 = xr - yr, a1 = xi - yi;
-            ea = fma(a0, a0, fma(a1, a1, ea));
-            a0 = xr - yi; a1 = xi + yr;
-            eb = fma(a0, a0, fma(a1, a1, eb));
-            a0 = xr + yi; a1 = xi - yr;
-            ec = fma(a0, a0, fma(a1, a1, ec));
-          }
-          da = ea; db = eb; dc = ec;
-        }
-        T ka = T(0), kb = T(0), kc = T(0);
-        if (live) {
-          ka = exp_fast(-fmax(da, T(0)) * inv2s);
-          kb = exp_fast(-fmax(db, T(0)) * inv2s);
-          kc = exp_fast(-fmax(dc, T(0)) * inv2s);
-        }
-        const T* cp = cs + p * 2 * KT;
-#pragma unroll
-        for (int u = 0; u < KT; ++u) {
-          const T c1 = cp[2 * u], c2 = cp[2 * u + 1];
-          are[u] = fma(c1, ka, fma(c2, kc, are[u]));
-          aim[u] = fma(c1, kb, fma(c2, ka, aim[u]));
-        }
-      }
+    for (; p < pc; p += DT_WARPS) {
+      const T* xp = xs + p * 2 * MT;
+      T crp, cip;
+      cdot<T, MT>(xp, y, crp, cip);
+      const T np_ = nxs[p];
+      const T dp = np_ + ny - T(2) * fmax(crp, fabs(cip));
+      const bool lp = tvalid && dp * inv2s < Thresh<T>::dead;
+      if (__any_sync(0xffffffffu, lp))
+        pair_update<T, MT, KT>(xp, np_, cs + p * 2 * KT, y, ny, crp, cip, tvalid, inv2s, are, aim);
     }
   }
   __syncthreads();
@@ -224,7 +281,13 @@ int launch_detect(const T* rx, long long rx_stride, int F, int K, int n_train, i
                   const T* coeff, const T* theta, kapsm_kernel_params p, const T* points,
                   int n_points, int bps, const unsigned char* tx, T* est, unsigned char* labels,
                   unsigned long long* be, unsigned long long* se, cudaStream_t s) {
-  size_t chunk = (size_t)DT_PC * (2 * MT + 1 + 2 * KT) * sizeof(T);
+  // pilot chunk: as many pilots as fit in ~100 KB (two CTAs per SM), multiple of 8
+  const size_t per_pilot = (2 * MT + 1 + 2 * KT) * sizeof(T);
+  int PC = (int)((100 * 1024 - 128 * sizeof(T)) / per_pilot);
+  PC = PC / 8 * 8;
+  if (PC > n_train) PC = (n_train + 7) / 8 * 8;
+  if (PC < 8) PC = 8;
+  size_t chunk = (size_t)PC * per_pilot + 16;
   size_t redb = (size_t)DT_WARPS * KT * 2 * 32 * sizeof(T);
   size_t smem = 128 * sizeof(T) + (chunk > redb ? chunk : redb);
   auto kern = detect_frames_kernel<T, MT, KT>;
@@ -232,7 +295,7 @@ int launch_detect(const T* rx, long long rx_stride, int F, int K, int n_train, i
       cudaSuccess)
     return KAPSM_ERR_CUDA;
   dim3 grid((n_data + 31) / 32, F);
-  kern<<<grid, DT_WARPS * 32, smem, s>>>(rx, rx_stride, K, n_train, n_data, M, coeff, theta,
+  kern<<<grid, DT_WARPS * 32, smem, s>>>(rx, rx_stride, K, n_train, n_data, M, PC, coeff, theta,
                                          (T)p.w_g, (T)(1.0 / (2.0 * p.sigma_sq)), points,
                                          n_points, bps, tx, est, labels, be, se);
   return status_from(cudaGetLastError());

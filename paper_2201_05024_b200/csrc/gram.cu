@@ -22,8 +22,9 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
                       T w_l, T w_g, T inv2s, T* __restrict__ gram, long long ld,
                       long long gram_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* xa = reinterpret_cast<T*>(smem_raw);        // [GRAM_TILE][2M]
-  T* xb = xa + GRAM_TILE * 2 * M;                // [GRAM_TILE][2M]
+  const int rs = 2 * M + 1;                       // odd row stride: conflict-free
+  T* xa = reinterpret_cast<T*>(smem_raw);        // [GRAM_TILE][rs]
+  T* xb = xa + GRAM_TILE * rs;                   // [GRAM_TILE][rs]
   const int f = blockIdx.z;
   const T* X = rx + (long long)f * rx_stride;
   const int p0 = blockIdx.y * GRAM_TILE, q0 = blockIdx.x * GRAM_TILE;
@@ -31,46 +32,61 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
   const int row_elems = 2 * M;
   for (int e = tid; e < GRAM_TILE * row_elems; e += GRAM_TILE * GRAM_TILE) {
     int r = e / row_elems, c = e - r * row_elems;
-    xa[e] = (p0 + r < n_train) ? X[(long long)(p0 + r) * row_elems + c] : T(0);
-    xb[e] = (q0 + r < n_train) ? X[(long long)(q0 + r) * row_elems + c] : T(0);
+    xa[r * rs + c] = (p0 + r < n_train) ? X[(long long)(p0 + r) * row_elems + c] : T(0);
+    xb[r * rs + c] = (q0 + r < n_train) ? X[(long long)(q0 + r) * row_elems + c] : T(0);
   }
   __syncthreads();
   const int p = p0 + threadIdx.y, q = q0 + threadIdx.x;
   if (p >= n_train || q >= n_train) return;
-  const T* x = xa + threadIdx.y * row_elems;
-  const T* y = xb + threadIdx.x * row_elems;
-  T s_rr = 0, s_ii = 0, s_ri = 0, s_ir = 0, d_a = 0, d_b = 0, d_c = 0;
+  const T* x = xa + threadIdx.y * rs;
+  const T* y = xb + threadIdx.x * rs;
+  T s_rr = 0, s_ii = 0, s_ri = 0, s_ir = 0, nx = 0, ny = 0;
   for (int k = 0; k < M; ++k) {
     const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
     s_rr = fma(xr, yr, s_rr);
     s_ii = fma(xi, yi, s_ii);
     s_ri = fma(xr, yi, s_ri);
     s_ir = fma(xi, yr, s_ir);
-    T a0, a1;
-    if constexpr (sizeof(T) == 4) {
-      a0 = __fsub_rn(xr, yr); a1 = __fsub_rn(xi, yi);
-      d_a = __fadd_rn(d_a, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
-      a0 = __fsub_rn(xr, yi); a1 = __fadd_rn(xi, yr);                 // x + i y
-      d_b = __fadd_rn(d_b, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
-      a0 = __fadd_rn(xr, yi); a1 = __fsub_rn(xi, yr);                 // x - i y
-      d_c = __fadd_rn(d_c, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
-    } else {
-      a0 = __dsub_rn(xr, yr); a1 = __dsub_rn(xi, yi);
-      d_a = __dadd_rn(d_a, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
-      a0 = __dsub_rn(xr, yi); a1 = __dadd_rn(xi, yr);
-      d_b = __dadd_rn(d_b, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
-      a0 = __dadd_rn(xr, yi); a1 = __dsub_rn(xi, yr);
-      d_c = __dadd_rn(d_c, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
-    }
+    nx = fma(xr, xr, fma(xi, xi, nx));
+    ny = fma(yr, yr, fma(yi, yi, ny));
   }
   const T lin_re = s_rr + s_ii;          // Re(x^H y)
   const T lin_12 = s_ri - s_ir;          // r1(x).r2(y)
   const T lin_21 = s_ir - s_ri;          // r2(x).r1(y)
   T g_a = 0, g_b = 0, g_c = 0;
   if (w_g != T(0)) {
-    g_a = exp_acc(-d_a * inv2s);
-    g_b = exp_acc(-d_b * inv2s);
-    g_c = exp_acc(-d_c * inv2s);
+    // Underflow screen from the (symmetric) norm expansion: if even a generous
+    // lower bound of every distance puts exp() below the smallest denormal,
+    // the Gaussian terms are exactly 0 and the exact pass is skipped.
+    const T nn = nx + ny;
+    const T dmin = nn - T(2) * fmax(lin_re, fmax(lin_12, lin_21));
+    const T slack = nn * (sizeof(T) == 4 ? T(1e-5) : T(1e-12));
+    const T dead = sizeof(T) == 4 ? T(104) : T(746);
+    if ((dmin - slack) * inv2s < dead) {
+      T d_a = 0, d_b = 0, d_c = 0;
+      for (int k = 0; k < M; ++k) {
+        const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+        T a0, a1;
+        if constexpr (sizeof(T) == 4) {
+          a0 = __fsub_rn(xr, yr); a1 = __fsub_rn(xi, yi);
+          d_a = __fadd_rn(d_a, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+          a0 = __fsub_rn(xr, yi); a1 = __fadd_rn(xi, yr);                 // x + i y
+          d_b = __fadd_rn(d_b, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+          a0 = __fadd_rn(xr, yi); a1 = __fsub_rn(xi, yr);                 // x - i y
+          d_c = __fadd_rn(d_c, __fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)));
+        } else {
+          a0 = __dsub_rn(xr, yr); a1 = __dsub_rn(xi, yi);
+          d_a = __dadd_rn(d_a, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+          a0 = __dsub_rn(xr, yi); a1 = __dadd_rn(xi, yr);
+          d_b = __dadd_rn(d_b, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+          a0 = __dadd_rn(xr, yi); a1 = __dsub_rn(xi, yr);
+          d_c = __dadd_rn(d_c, __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)));
+        }
+      }
+      g_a = exp_acc(-d_a * inv2s);
+      g_b = exp_acc(-d_b * inv2s);
+      g_c = exp_acc(-d_c * inv2s);
+    }
   }
   const T k11 = w_l * lin_re + w_g * g_a;
   const T k12 = w_l * lin_12 + w_g * g_b;
@@ -93,7 +109,7 @@ int pilot_gram(const T* rx, long long rx_stride, int F, int n_train, int M,
   if (F == 0 || n_train == 0) return KAPSM_OK;
   const int nt = (n_train + GRAM_TILE - 1) / GRAM_TILE;
   dim3 grid(nt, nt, F), block(GRAM_TILE, GRAM_TILE);
-  size_t smem = 2 * GRAM_TILE * 2 * (size_t)M * sizeof(T);
+  size_t smem = 2 * GRAM_TILE * (2 * (size_t)M + 1) * sizeof(T);
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(pilot_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
@@ -113,22 +129,23 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
     sample_gram_kernel(const T* __restrict__ S, long long s_stride, int N, int D, T w_l, T w_g,
                        T inv2s, T* __restrict__ gram, long long ld, long long gram_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sa = reinterpret_cast<T*>(smem_raw);   // [GRAM_TILE][D]
-  T* sb = sa + GRAM_TILE * D;
+  const int rs = D | 1;                     // odd row stride: conflict-free
+  T* sa = reinterpret_cast<T*>(smem_raw);   // [GRAM_TILE][rs]
+  T* sb = sa + GRAM_TILE * rs;
   const int f = blockIdx.z;
   const T* Sf = S + (long long)f * s_stride;
   const int i0 = blockIdx.y * GRAM_TILE, j0 = blockIdx.x * GRAM_TILE;
   const int tid = threadIdx.y * GRAM_TILE + threadIdx.x;
   for (int e = tid; e < GRAM_TILE * D; e += GRAM_TILE * GRAM_TILE) {
     int r = e / D, c = e - r * D;
-    sa[e] = (i0 + r < N) ? Sf[(long long)(i0 + r) * D + c] : T(0);
-    sb[e] = (j0 + r < N) ? Sf[(long long)(j0 + r) * D + c] : T(0);
+    sa[r * rs + c] = (i0 + r < N) ? Sf[(long long)(i0 + r) * D + c] : T(0);
+    sb[r * rs + c] = (j0 + r < N) ? Sf[(long long)(j0 + r) * D + c] : T(0);
   }
   __syncthreads();
   const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
   if (i >= N || j >= N) return;
-  const T* a = sa + threadIdx.y * D;
-  const T* b = sb + threadIdx.x * D;
+  const T* a = sa + threadIdx.y * rs;
+  const T* b = sb + threadIdx.x * rs;
   T dot = T(0), d2 = T(0);
   for (int k = 0; k < D; ++k) {
     dot = fma(a[k], b[k], dot);
@@ -147,7 +164,7 @@ int sample_gram(const T* S, long long s_stride, int F, int N, int D, kapsm_kerne
   if (F == 0 || N == 0) return KAPSM_OK;
   const int nt = (N + GRAM_TILE - 1) / GRAM_TILE;
   dim3 grid(nt, nt, F), block(GRAM_TILE, GRAM_TILE);
-  size_t smem = 2 * GRAM_TILE * (size_t)D * sizeof(T);
+  size_t smem = 2 * GRAM_TILE * (size_t)(D | 1) * sizeof(T);
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(sample_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
