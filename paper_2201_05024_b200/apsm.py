@@ -192,7 +192,9 @@ def apsm_step(f: FilterState, window: Sequence[TrainingSample], cfg: ApsmConfig)
 # ---------------------------------------------------------------------------
 
 def _ld(n: int) -> int:
-    return max(32, (n + 31) // 32 * 32)
+    """Gram row stride: 16-byte aligned rows with >= 16 bytes of padding past the
+    last sample (the trainer's TMA row copies round up to 16 bytes)."""
+    return (n + 8 + 31) // 32 * 32
 
 
 def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,

@@ -27,7 +27,9 @@ __all__ = ["FramePipeline", "host_frames"]
 
 
 def _ld(n: int) -> int:
-    return max(32, (n + 31) // 32 * 32)
+    """Gram row stride: 16-byte aligned rows with >= 16 bytes of padding past the
+    last sample (the trainer's TMA row copies round up to 16 bytes)."""
+    return (n + 8 + 31) // 32 * 32
 
 
 class FramePipeline:
