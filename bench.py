@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 APSM detector hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): the paper scenario -- 6
+NOMA users, 16 Rx antennas, QPSK, 685 pilot + 3840 data symbols per OFDM
+frame, 20 dB, APSM W=20, eps=0.01, w_l=w_g=0.5, sigma^2=0.05 -- one frame per
+step per GPU: train every user on the frame's pilots, detect the payload,
+decide, count errors (K1 Gram -> K2 persistent trainer -> K3 fused detect,
+replayed as a CUDA graph).  Frames are seeded synthetic frames generated with
+the reference's own RNG order, drawn from a device-resident pool larger than
+L2 (distinct input every step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun, one process per GPU): each rank processes its own frames
+(weak scaling); per step the decisions are all-gathered and the error
+counters all-reduced over NCCL.  value = frames/s of the whole job, timed with
+CUDA events, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")   # one BLAS thread per CPU worker process
+
+METRIC = ("per-OFDM-frame train+detect latency p50/p99 (µs); detected frames/sec at "
+          "1/2/4/8 B200")
+UNIT = "frames/s"
+K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME = 6, 16, 685, 3840, "QPSK"
+W_WIN = 20
+WORKLOAD = "paper scenario C1/C2: 6 users QPSK, 16 Rx, 685 pilots + 3840 data symbols, 1 frame/step/GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--pool", type=int, default=256, help="distinct frames per rank (> L2)")
+    ap.add_argument("--lat-samples", type=int, default=1000)
+    ap.add_argument("--throughput-frames", type=int, default=296)
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per frame (minimal shared-Gram model)
+# ---------------------------------------------------------------------------
+def flops_per_frame(K=K_USERS, M=M_ANT, n_train=N_TRAIN, n_data=N_DATA, W=W_WIN):
+    D, Np, Nd = 2 * M, 2 * n_train, 2 * n_data
+    f_gram = Np * (Np - 1) / 2 * (2 * D + 6)
+    f_seq = K * (Np ** 2 + 2 * Np * W ** 2)
+    f_det = Np * Nd * (2 * D + 4) + 2 * K * Np * Nd + 2 * K * Nd * D
+    return dict(gram=f_gram, train=f_seq, detect=f_det, total=f_gram + f_seq + f_det)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        import statistics
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the reference package from baseline/_ref, else the oracle port)
+# ---------------------------------------------------------------------------
+def _cpu_kind():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "kapsm")):
+        return "reference", ref
+    return "port", None
+
+
+def _cpu_task(args):
+    """train + batch_detect + demodulate_hard + ber for one (frame, user), 1 thread."""
+    seed, user = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    kind, ref = _cpu_kind()
+    import numpy as np
+    t0 = time.perf_counter()
+    if kind == "reference":
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import kapsm
+        rng = np.random.default_rng([seed, 1, M_ANT])
+        ch = kapsm.draw_channel(K_USERS, M_ANT, "uniform", kapsm.noise_var_for_snr(np.ones(K_USERS), 20.0), rng)
+        bits = rng.integers(0, 2, size=(K_USERS, (N_TRAIN + N_DATA) * 2))
+        syms = np.stack([kapsm.modulate(bits[u], SCHEME) for u in range(K_USERS)])
+        rx = kapsm.synthesize_received(syms, ch, rng)
+        t0 = time.perf_counter()
+        f = kapsm.train(kapsm.zero_filter(2 * M_ANT), zip(rx[:N_TRAIN], syms[user, :N_TRAIN]), kapsm.ApsmConfig())
+        est = kapsm.batch_detect(f, rx[N_TRAIN:], kapsm.KernelParams(),
+                                 kapsm.EngineConfig(stage="balanced", tile_inputs=256))
+        rb = kapsm.demodulate_hard(est, SCHEME)
+        err = int(np.sum(rb != bits[user, N_TRAIN * 2:]))
+    else:
+        from oracle import kapsm_oracle as O
+        fr = O.make_frame(seed, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME)
+        t0 = time.perf_counter()
+        err = O.run_frame(fr, N_TRAIN, SCHEME, users=[user])[0]["bit_err"]
+    return time.perf_counter() - t0, err
+
+
+def _noop(_):
+    import numpy  # noqa: F401
+    return 0
+
+
+def cpu_run(frames, procs):
+    """Process pool over (frame, user) tasks; returns (wall_s, task_times, errors)."""
+    import multiprocessing as mp
+    tasks = [(s, u) for s in frames for u in range(K_USERS)]
+    ctx = mp.get_context("spawn")          # the parent holds a CUDA context: do not fork
+    with ctx.Pool(procs) as pool:
+        pool.map(_noop, range(procs))      # start-up (imports) outside the timing
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_task, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+    return wall, [r[0] for r in res], sum(r[1] for r in res)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    kind, _ = _cpu_kind()
+    cores = cpu_cores()
+    procs = max(1, min(cores, K_USERS))
+    # one step = one frame (all users in parallel); a single user per step when
+    # K is large so that the whole run stays within a few minutes
+    per_step_users = K_USERS if args.steps + args.warmup <= 60 else 1
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    times = []
+    errs = 0
+    with ctx.Pool(procs) as pool:
+        for i in range(args.warmup + args.steps):
+            tasks = [(100000 + i, u) for u in range(per_step_users)]
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_task, tasks, chunksize=1)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                errs += sum(r[1] for r in res)
+    import numpy as np
+    tot = float(np.sum(times))
+    frames = len(times) * per_step_users / K_USERS
+    value = frames / tot
+    lat = np.array(times) * (K_USERS / per_step_users) * 1e6
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic (seeded, reference RNG order)",
+          "config": {"workload": WORKLOAD, "users_per_step": per_step_users,
+                     "engine": "balanced, tile_inputs=256, workers=1 per process"},
+          "latency_us": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                         "n": int(lat.size), "note": "per-frame wall time, users in parallel"},
+          "bit_errors": int(errs),
+          "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind,
+                           "sample": f"{per_step_users} user(s) x {len(times)} steps, one process per user"},
+          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2201_05024_b200 as K
+    from paper_2201_05024_b200 import _device as dv, _lib
+    from paper_2201_05024_b200 import dist as D
+
+    info = D.init_from_env()
+    world, rank = info.world, info.rank
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- frame pool (distinct seeds per rank, > L2) ----------------
+    P = args.pool
+    seeds = [rank * 1_000_000 + i for i in range(P)]
+    rx_h, pil_h, tx_h, bits_h = K.host_frames(seeds, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME)
+    T = N_TRAIN + N_DATA
+    rx_f = np.ascontiguousarray(np.stack([rx_h.real, rx_h.imag], -1).astype(np.float32))
+    pil_f = np.ascontiguousarray(np.stack([pil_h.real, pil_h.imag], -1).astype(np.float32))
+    tx_u8 = np.ascontiguousarray(tx_h.astype(np.uint8))
+    rx_pin = torch.from_numpy(rx_f).pin_memory()
+    pil_pin = torch.from_numpy(pil_f).pin_memory()
+    tx_pin = torch.from_numpy(tx_u8).pin_memory()
+    rx_d, pil_d, tx_d = rx_pin.to(dev), pil_pin.to(dev), tx_pin.to(dev)
+    pool_bytes = rx_d.numel() * 4 + pil_d.numel() * 4 + tx_d.numel()
+
+    pipe = K.FramePipeline(1, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32",
+                           store_est=False)
+    pipe.load(rx_d[0:1], pil_d[0:1], tx_d[0:1])
+    pipe.capture()
+    torch.cuda.synchronize()
+
+    lab_g = None
+
+    def step(i):
+        j = i % P
+        pipe.rx.copy_(rx_d[j:j + 1], non_blocking=True)
+        pipe.pilots.copy_(pil_d[j:j + 1], non_blocking=True)
+        pipe.tx.copy_(tx_d[j:j + 1], non_blocking=True)
+        pipe.replay()
+        if world > 1:
+            D.gather_decisions(pipe.labels)
+            D.reduce_counts(pipe.bit_err)
+
+    # ---------------- timed region: exactly K steps ----------------
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e_all0.record()
+    for i in range(args.steps):
+        ev[i][0].record()
+        step(args.warmup + i)
+        ev[i][1].record()
+    e_all1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    total_ms = e_all0.elapsed_time(e_all1)
+    step_us = np.array([a.elapsed_time(b) * 1e3 for a, b in ev])
+    total_ms_max = max_over_ranks(total_ms)
+    value = world * args.steps / (total_ms_max / 1e3)
+    bit_err_last = int(pipe.bit_err.sum().item())
+
+    # ---------------- latency distribution: graph replays on resident frames ----------------
+    lat = []
+    for i in range(args.lat_samples):
+        j = i % P
+        pipe.rx.copy_(rx_d[j:j + 1]); pipe.pilots.copy_(pil_d[j:j + 1]); pipe.tx.copy_(tx_d[j:j + 1])
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); pipe.replay(); b.record()
+        lat.append((a, b))
+    torch.cuda.synchronize()
+    lat_us = np.array([a.elapsed_time(b) * 1e3 for a, b in lat])
+
+    # ---------------- per-kernel times (roofline) ----------------
+    def kernel_times(reps=20):
+        c = pipe.cfg
+        p = _lib.params(c.params)
+        st = dv.stream()
+        acc = np.zeros(3)
+        for _ in range(reps):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record()
+            _lib.check(dv.fn("kapsm_pilot_gram", "f32")(dv.ptr(pipe.rx), T * M_ANT * 2, 1, N_TRAIN, M_ANT, p, dv.ptr(pipe.gram), pipe.ld, pipe.Np * pipe.ld, st), "gram")
+            e[1].record()
+            _lib.check(dv.fn("kapsm_train", "f32")(dv.ptr(pipe.gram), pipe.ld, pipe.Np * pipe.ld, dv.ptr(pipe.rx), T * M_ANT * 2, dv.ptr(None), 0, 2 * M_ANT, dv.ptr(pipe.pilots), 1, K_USERS, pipe.Np, c.window, float(c.epsilon), p, dv.ptr(pipe.qtab), dv.ptr(None), dv.ptr(None), dv.ptr(pipe.coeff), dv.ptr(pipe.first_step), dv.ptr(pipe.theta), dv.ptr(pipe.n_active), dv.ptr(pipe.status), st), "train")
+            e[2].record()
+            _lib.check(dv.fn("kapsm_detect_frames", "f32")(dv.ptr(pipe.rx), T * M_ANT * 2, 1, K_USERS, N_TRAIN, N_DATA, M_ANT, dv.ptr(pipe.coeff), dv.ptr(pipe.theta), p, dv.ptr(pipe.points), pipe.n_points, pipe.bps, dv.ptr(pipe.tx), dv.ptr(None), dv.ptr(pipe.labels), dv.ptr(pipe.bit_err), dv.ptr(pipe.sym_err), st), "detect")
+            e[3].record()
+            e[3].synchronize()
+            acc += [e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])]
+        return acc / reps * 1e3   # us
+
+    kt = kernel_times()
+
+    # FP32 SIMT peak (measured here; MEASURED_PEAKS.json has HBM and bf16 only)
+    fn = lib.kapsm_internal_fp32_peak
+    import ctypes as C
+    fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    sink = torch.zeros(148 * 64, dtype=torch.float32, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, iters = nsm * 8, 4096
+    _lib.check(fn(dv.ptr(sink), 64, blocks, dv.stream()), "peak")
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    _lib.check(fn(dv.ptr(sink), iters, blocks, dv.stream()), "peak")
+    b.record()
+    b.synchronize()
+    fp32_peak = blocks * 256 * iters * 64 * 2 / (a.elapsed_time(b) / 1e3) / 1e12
+
+    fl = flops_per_frame()
+    names = ["pilot_gram", "apsm_train", "detect_frames"]
+    fkeys = ["gram", "train", "detect"]
+    per_kernel = {n: {"us": float(t), "algorithmic_gflop": fl[k] / 1e9,
+                      "tflops": fl[k] / (t / 1e6) / 1e12,
+                      "frac_of_fp32_peak": fl[k] / (t / 1e6) / 1e12 / fp32_peak}
+                  for n, t, k in zip(names, kt, fkeys)}
+    dom = int(np.argmax(kt))
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(names[dom] + "_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "kernel": names[dom],
+                "achieved": per_kernel[names[dom]]["tflops"], "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": per_kernel[names[dom]]["frac_of_fp32_peak"],
+                "traffic": traffic,
+                "peak_source": "measured on this GPU (FFMA probe, 3-register form)",
+                "note": ("apsm_train is a 1370-step sequential chain per user (latency-bound); "
+                         "algorithmic FLOPs per SURVEY 8(d) minimal model"),
+                "kernels": per_kernel}
+
+    # ---------------- end to end through the public API (host buffers) ----------------
+    lab_h = torch.empty((1, K_USERS, N_DATA), dtype=torch.uint8).pin_memory()
+    cnt_h = torch.empty((2, 1, K_USERS), dtype=torch.int64).pin_memory()
+    h2d = rx_pin[0:1].numel() * 4 + pil_pin[0:1].numel() * 4 + tx_pin[0:1].numel()
+    d2h = lab_h.numel() + cnt_h.numel() * 8
+
+    def e2e_step(i):
+        j = i % P
+        pipe.load(rx_pin[j:j + 1], pil_pin[j:j + 1], tx_pin[j:j + 1], non_blocking=True)
+        pipe.replay()
+        if world > 1:
+            D.gather_decisions(pipe.labels)
+            D.reduce_counts(pipe.bit_err)
+        lab_h.copy_(pipe.labels, non_blocking=True)
+        cnt_h[0].copy_(pipe.bit_err, non_blocking=True)
+        cnt_h[1].copy_(pipe.sym_err, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(args.steps):
+        e2e_step(i)
+    b.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(a.elapsed_time(b))
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
+
+    # ---------------- throughput mode: many frames per launch ----------------
+    thr = None
+    Ft = args.throughput_frames
+    if Ft > 0:
+        Ft = min(Ft, P)
+        tp = K.FramePipeline(Ft, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32",
+                             store_est=False)
+        tp.load(rx_d[:Ft], pil_d[:Ft], tx_d[:Ft])
+        tp.capture()
+        for _ in range(2):
+            tp.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        a.record()
+        for _ in range(reps):
+            tp.replay()
+        b.record()
+        b.synchronize()
+        ms = max_over_ranks(a.elapsed_time(b) / reps)
+        thr = {"frames_per_launch": Ft, "frames_per_s": world * Ft / (ms / 1e3),
+               "ms_per_launch": ms, "bit_errors": int(tp.bit_err.sum().item())}
+        del tp
+
+    # ---------------- CPU baseline (rank 0, N = 1) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        kind, _ = _cpu_kind()
+        procs = max(1, min(cpu_cores(), K_USERS * args.cpu_frames))
+        wall, ttimes, cerr = cpu_run([200000 + i for i in range(args.cpu_frames)], procs)
+        cpu = {"value": args.cpu_frames / wall, "unit": UNIT, "cores": procs, "kind": kind,
+               "sample": (f"{args.cpu_frames} frames x {K_USERS} users as (frame,user) tasks over "
+                          f"{procs} processes (1 thread each); reference train + batch_detect("
+                          "balanced, tile_inputs=256) + demodulate_hard + ber"),
+               "latency_us_single_process": float(np.sum(ttimes) / args.cpu_frames * 1e6),
+               "bit_errors": int(cerr)}
+
+    if rank == 0:
+        launches_per_step = 3      # pilot_gram, apsm_train, detect_frames
+        emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+              "steps": args.steps, "warmup": args.warmup,
+              "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+              "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+              "data": "synthetic (seeded frames, reference RNG order)",
+              "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": 1,
+                         "pool_frames_per_gpu": P, "pool_bytes": int(pool_bytes),
+                         "l2": "input pool > L2 (distinct frame every step)",
+                         "window": W_WIN, "parallelism": f"dp{world} (independent frames)"},
+              "latency_us": {"p50": float(np.percentile(lat_us, 50)),
+                             "p99": float(np.percentile(lat_us, 99)),
+                             "mean": float(lat_us.mean()), "n": int(lat_us.size),
+                             "timed_steps_p50": float(np.percentile(step_us, 50)),
+                             "timed_steps_p99": float(np.percentile(step_us, 99)),
+                             "budget_us": 1000.0},
+              "roofline": roofline,
+              "cpu_baseline": cpu,
+              "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(d2h)},
+              "throughput_mode": thr,
+              "gpu_launches": launches_per_step * args.steps,
+              "bit_errors_last_step": bit_err_last,
+              "clocks": clk})
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -658,3 +658,31 @@ extern "C" const char* kapsm_strerror(int code) {
   }
 }
 extern "C" int kapsm_abi_version(void) { return 100; }
+
+// ---------------------------------------------------------------------------
+// Internal instrumentation: FP32 FFMA throughput probe (the SIMT roofline
+// denominator; MEASURED_PEAKS.json has only HBM and bf16 tensor peaks).
+// Each thread runs 8 independent FFMA chains, 64 FFMA per iteration.
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0f + 1e-6f * (threadIdx.x + k);
+  // register operands (3-register FFMA form, as in the real kernels)
+  const float b = 0.999999f - 1e-9f * threadIdx.x, c = 1e-7f * (1 + (threadIdx.x & 3));
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.f) out[blockIdx.x] = s;   // keep the work alive
+}
+extern "C" int kapsm_internal_fp32_peak(float* out, int iters, int blocks, void* stream) {
+  if (!out || iters < 1 || blocks < 1) return KAPSM_ERR_INVALID;
+  fp32_peak_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
+  return status_from(cudaGetLastError());
+}

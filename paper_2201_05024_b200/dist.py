@@ -1,0 +1,81 @@
+"""Multi-GPU frame sharding (one process per GPU, torch.distributed over NCCL).
+
+Frames are independent: every rank runs the whole K1 -> K2 ->
+K3 pipeline on its own frames with no exchange during compute.  The only
+collective step gathers the hard decisions and reduces the error counters:
+
+* ``all_gather_into_tensor`` of the uint8 decision labels (F_local x K x n_data
+  per rank),
+* ``all_reduce(SUM)`` of the int64 per-user bit / symbol error counters.
+
+The same functions run on the ``gloo`` backend with CPU tensors (tests).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+import torch.distributed as tdist
+
+__all__ = ["RankInfo", "init_from_env", "shard_frames", "gather_decisions", "reduce_counts"]
+
+
+@dataclass(frozen=True)
+class RankInfo:
+    rank: int
+    world: int
+    local_rank: int
+
+    @property
+    def is_root(self) -> bool:
+        return self.rank == 0
+
+
+def init_from_env(backend: Optional[str] = None) -> RankInfo:
+    """Initialise the default process group from torchrun's environment
+    (RANK, WORLD_SIZE, LOCAL_RANK, MASTER_ADDR/PORT).  Single process when the
+    variables are absent."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not tdist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            tdist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return RankInfo(rank, world, local)
+
+
+def shard_frames(frame_ids: Sequence[int], rank: int, world: int) -> list:
+    """Round-robin partition of independent frames over ranks (frame f -> rank
+    f mod world); disjoint and covering."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    return [f for i, f in enumerate(frame_ids) if i % world == rank]
+
+
+def gather_decisions(labels: torch.Tensor, group=None) -> torch.Tensor:
+    """All ranks' decision tensors stacked along a new leading rank axis."""
+    world = tdist.get_world_size(group) if tdist.is_initialized() else 1
+    if world == 1:
+        return labels.unsqueeze(0)
+    x = labels.contiguous()
+    out = torch.empty((world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    tdist.all_gather_into_tensor(out, x, group=group)
+    return out.view((world,) + tuple(x.shape))
+
+
+def reduce_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the per-user error counters over ranks (in place, returned)."""
+    if tdist.is_initialized() and tdist.get_world_size(group) > 1:
+        tdist.all_reduce(counts, op=tdist.ReduceOp.SUM, group=group)
+    return counts
