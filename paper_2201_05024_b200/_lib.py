@@ -61,6 +61,8 @@ SIGNATURES = {
     "kapsm_demap_f32": (_I, [_P, _LL, _P, _I, _P, _P]),
     "kapsm_demap_f64": (_I, [_P, _LL, _P, _I, _P, _P]),
     "kapsm_count_mismatch": (_I, [_P, _P, _LL, _I, _P, _P]),
+    # internal instrumentation (not in the public header)
+    "kapsm_internal_fp32_peak": (_I, [_P, _I, _I, _P]),
 }
 
 _lib = None
