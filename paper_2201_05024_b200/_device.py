@@ -47,5 +47,9 @@ def fn(name: str, prec: str):
     return getattr(_lib.load(), f"{name}_{prec}")
 
 
+def zeros(shape, prec: str):
+    return torch.zeros(shape, dtype=DTYPES[prec][0], device=device())
+
+
 def empty(shape, prec: str):
     return torch.empty(shape, dtype=DTYPES[prec][0], device=device())

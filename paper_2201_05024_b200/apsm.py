@@ -192,9 +192,10 @@ def apsm_step(f: FilterState, window: Sequence[TrainingSample], cfg: ApsmConfig)
 # ---------------------------------------------------------------------------
 
 def _ld(n: int) -> int:
-    """Gram row stride: 16-byte aligned rows with >= 16 bytes of padding past the
-    last sample (the trainer's TMA row copies round up to 16 bytes)."""
-    return (n + 8 + 31) // 32 * 32
+    """Gram row stride: 128-byte aligned rows with >= 16 zero columns past the
+    last sample (the trainer's TMA copies read whole 16-byte granules and the
+    staged column segments run up to 11 columns past the last sample)."""
+    return (n + 16 + 31) // 32 * 32
 
 
 def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,
@@ -223,7 +224,7 @@ def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,
             f"window {cfg.window} / {N} realified samples exceed this build's trainer limits "
             f"(window <= {lib.kapsm_max_window()}, samples <= {lib.kapsm_max_samples()})")
     ld = _ld(N)
-    gram = dv.empty((N, ld), prec)
+    gram = dv.zeros((N, ld), prec)
     if rx_pilots is not None:
         _lib.check(dv.fn("kapsm_pilot_gram", prec)(dv.ptr(rxd), N * M, 1, T, M, kp, dv.ptr(gram),
                                                    ld, N * ld, st), "pilot_gram")

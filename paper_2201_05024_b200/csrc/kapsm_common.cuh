@@ -133,3 +133,135 @@ KAPSM_DEV bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
 }
 
 }  // namespace kapsm
+
+namespace kapsm {
+
+// ---- explicit shared-space accesses (32-bit shared addresses; no generic
+//      address materialisation on the trainer's critical path) ----
+KAPSM_DEV void sts(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+KAPSM_DEV void sts(unsigned a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+KAPSM_DEV float4 lds_f4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+KAPSM_DEV double2 lds_d2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+KAPSM_DEV float lds_f(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+KAPSM_DEV double lds_d(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+template <typename T> KAPSM_DEV T lds_t(unsigned a);
+template <> KAPSM_DEV float lds_t<float>(unsigned a) { return lds_f(a); }
+template <> KAPSM_DEV double lds_t<double>(unsigned a) { return lds_d(a); }
+
+// cp.async of one scalar to a 32-bit shared address
+template <typename T>
+KAPSM_DEV void cp_async_s(unsigned d, const T* gmem_src) {
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+
+}  // namespace kapsm
+
+namespace kapsm {
+
+// opaque copy: the compiler can neither rematerialise nor fold the value
+KAPSM_DEV unsigned opaque_u32(unsigned v) {
+  unsigned r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+KAPSM_DEV void sts_i(unsigned a, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+KAPSM_DEV int lds_i(unsigned a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+KAPSM_DEV float2 lds_f2(unsigned a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+template <typename T> KAPSM_DEV void lds_pair(unsigned a, T& x, T& y);
+template <> KAPSM_DEV void lds_pair<float>(unsigned a, float& x, float& y) {
+  const float2 v = lds_f2(a); x = v.x; y = v.y;
+}
+template <> KAPSM_DEV void lds_pair<double>(unsigned a, double& x, double& y) {
+  const double2 v = lds_d2(a); x = v.x; y = v.y;
+}
+
+// tagged slots addressed by 32-bit shared addresses (layout as Tagged<T>)
+KAPSM_DEV void st_tag(unsigned a, float v, int tag) {
+  unsigned long long w = ((unsigned long long)(unsigned)tag << 32) | __float_as_uint(v);
+  asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(a), "l"(w) : "memory");
+}
+KAPSM_DEV void st_tag(unsigned a, double v, int tag) {
+  asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(__double_as_longlong(v)),
+               "l"((unsigned long long)(unsigned)tag)
+               : "memory");
+}
+KAPSM_DEV bool ld_tag(unsigned a, int tag, float& v) {
+  unsigned long long w;
+  asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
+  v = __uint_as_float((unsigned)(w & 0xffffffffu));
+  return (int)(w >> 32) == tag;
+}
+KAPSM_DEV bool ld_tag(unsigned a, int tag, double& v) {
+  unsigned long long x, t;
+  asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(t) : "r"(a) : "memory");
+  v = __longlong_as_double((long long)x);
+  return (int)t == tag;
+}
+
+}  // namespace kapsm
+
+namespace kapsm {
+KAPSM_DEV bool mbar_try_wait_s(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+}  // namespace kapsm
+
+namespace kapsm {
+// tagged slot read without the tag test (the caller compares later)
+KAPSM_DEV void ld_tagged(unsigned a, float& v, int& tag) {
+  unsigned long long w;
+  asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
+  v = __uint_as_float((unsigned)(w & 0xffffffffu));
+  tag = (int)(w >> 32);
+}
+KAPSM_DEV void ld_tagged(unsigned a, double& v, int& tag) {
+  unsigned long long x, t;
+  asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(t) : "r"(a) : "memory");
+  v = __longlong_as_double((long long)x);
+  tag = (int)t;
+}
+}  // namespace kapsm

@@ -1,6 +1,6 @@
-// K2: persistent APSM trainer.  One CTA per SM runs 4 independent chain
-// groups (one per SM sub-partition); each group trains one (frame, user) at a
-// time and loops over its share of the F*K tasks.
+// K2: persistent APSM trainer.  One chain group trains one (frame, user) at a
+// time: a CRITICAL warp runs the strictly sequential pilot loop, BACKGROUND
+// warps compute everything that does not depend on the current step.
 //
 // Reference semantics: ApsmTrainer.observe (apsm.py:304-359) driven by
 // train()/observe_symbol (apsm.py:361-396).  At step n (realified sample n),
@@ -10,138 +10,229 @@
 //   c_j  += q_j beta_j, q = uniform_weights(|J_n|)   (apsm.py:336-359)
 // where f_n = f0 + sum_i c_i kappa(r_i, .).  The represented function is the
 // reference's (collapsed theta + one atom per activated sample); theta is
-// formed at the end as w_l sum_i c_i r_i (the reference accumulates it per
-// step, apsm.py:338 -- same value up to summation order).
+// formed at the end as theta0 + w_l sum_i c_i r_i (the reference accumulates it
+// per step, apsm.py:338 -- same value up to summation order).
 //
-// Restatement used here (pilot Gram K from K1; all sums exact rearrangements
-// of the reference's window response):
-//   * every CRITICAL lane x owns one sample m (m = x mod 32) from step m-1 to
-//     step m+30, keeping Y_m (response), c_m, first_step_m in registers, and
-//     the slot-indexed column col2[x][l] = K[sample(l)][m] in shared memory;
-//   * window update after step n's betas (one 32-term dot per lane):
-//       Y_m += sum_l delta_l K[l][m]                      (m in J_n)
-//   * the entering sample n+1 gets its full response from the same dot with
-//     the coefficient vector instead of delta:
-//       Y_{n+1} = sum_l c_l^(n+1) K[l][n+1] + P_{n+1},
-//       P_m = f0(r_m) + sum_{i <= m-32} cfinal_i K[i][m];
-//   * P is computed by 3 BACKGROUND warps per group: final coefficients are
-//     published as tagged 64-bit words (value + index, no fence needed); warp
-//     k computes P_m for m = 32+k (mod 3) as one coalesced warp-wide dot over
-//     Gram row m as soon as c_{m-32} is final, and publishes it tagged, about
-//     S-W steps before the critical warp needs it;
-//   * taking over sample n+2 needs one Gram row segment (32 values), staged by
-//     cp.async TR_DELTA steps ahead; it refreshes one entry of every lane's
-//     column and the whole column of the new lane (symmetry).
-// Scheduling: group g = warp % 4 lives on sub-partition g; its critical warp
-// has the highest warp id there (the issue arbiter favours it) and there is
-// exactly one CTA per SM, so no foreign warp can starve a critical warp.
+// Restatement (pilot sum-kernel Gram K from K1; exact rearrangements):
+//   * slot x (= lane x of the critical warp) owns sample m = x (mod 32) from
+//     step m-L-1 (L = TC_L, the lookahead) until m leaves the window;
+//   * every owned sample accumulates the step's window update
+//         Y_m += sum_{l in J_n} delta_l K[l][m]            (one dot per lane)
+//     from its first owned step on, so that when it enters the window
+//         f(r_m) = init_m + Y_m,
+//         init_m = f0(r_m) + sum_{i<m} c_i^(n_m) K[i][m],  n_m = m-L-1,
+//     the coefficients c^(n_m) being those at the start of step n_m;
+//   * init_m is computed by the BACKGROUND warps: final coefficients
+//     (i <= m-32, published as tagged words when the sample leaves the window)
+//     dotted with the TMA-staged Gram row m, plus the 31 slot coefficients
+//     from a tagged per-step snapshot.  It is needed L+1 steps later;
+//   * the critical warp's step is therefore one chain
+//         Y -> delta = max(q/den (b-eps-f), 0) + min(q/den (b+eps-f), 0)
+//           -> smem broadcast -> window dot (registers x broadcast) -> Y
+//     with the slot rotation unrolled 32-wide so that every register index is
+//     static; the entering slot's Gram column arrives by cp.async TC_DELTA
+//     steps ahead.
+// Scheduling: one CTA per SM.  Latency mode (NG = 1): the critical warp is the
+// only warp on its SM sub-partition, six background warps on the other three.
+// Throughput mode (NG = 4): group g lives on sub-partition g, its critical
+// warp has the highest warp id there (the issue arbiter favours it).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdlib>
+#include <mutex>
 #include <type_traits>
 #include "kapsm_common.cuh"
 
 namespace kapsm {
 
-constexpr int TR_S = 32;           // critical slots (one warp)
-constexpr int TR_BGW = 3;          // background warps per group
-constexpr int TR_BGL = TR_BGW * 32;   // background lanes per group
-constexpr int TR_NJ = 16;          // P accumulators per background lane (registers)
-constexpr int TR_RB = 4;           // Gram rows in the TMA ring
-constexpr int TR_DELTA = 8;        // column prefetch distance (steps)
-constexpr int TR_PBN = 64;         // P slots (ring)
-constexpr int TR_CR = 64;          // final-coefficient slots (ring, power of 2)
-constexpr int TR_CSTR = TR_S + 4;  // col2 row stride: 16B rows, conflict-free LDS.128
-constexpr int TR_STG = 16;         // staged Gram rows (ring, power of 2 >= DELTA+2)
-constexpr int TR_MIN_LB = 7;       // minimum look-behind (background slack)
-constexpr int TR_MAX_W = TR_S - 1 - TR_MIN_LB;
-constexpr int TR_MAX_NP = TR_BGL * TR_NJ;
-constexpr long long TR_SPIN_LIMIT = 1LL << 26;
+constexpr int TC_S = 32;                    // slots (one warp)
+constexpr int TC_BT = 4;                    // batch: takeover / entry / publication every 4 steps
+constexpr int TC_MAX_W = 24;                // lookahead D >= 4 with D + W <= 29
+constexpr int TC_PF = 2;                    // column prefetch distance (batches)
+constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2 > PF)
+constexpr int TC_SNAP = 8;                  // coefficient snapshots (ring of batches)
+constexpr int TC_INIT = 64;                 // init values (ring, pow2)
+constexpr int TC_Q = 64;                    // init part A covers i <= m - Q
+constexpr int TC_LAG = 3;                   // background: part A runs LAG tasks ahead of B
+constexpr int TC_ARING = 4;                 // part-A results in flight per warp (> LAG)
+constexpr int TC_MAX_NP = 3072;
+// slot reuse: the batch taken over after step n (samples n+D..n+D+3) reuses
+// the slots of samples that left the window by step n: D + 3 + W - 33 <= 0.
+__host__ __device__ constexpr int lookahead(int wm) {
+  return ((30 - wm) & ~3) > 8 ? 8 : ((30 - wm) & ~3);
+}
+constexpr long long TC_SPIN_LIMIT = 1LL << 20;
 
-// 32-term dot of two 16-byte aligned shared-memory vectors (LDS.128, 4 chains)
-KAPSM_DEV float dot32(const float* a, const float* b) {
-  const float4* a4 = reinterpret_cast<const float4*>(a);
-  const float4* b4 = reinterpret_cast<const float4*>(b);
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+template <int K> using ic = std::integral_constant<int, K>;
+
+// ---- window dot: Yz + sum over the window lanes of delta_l * row[l] ----
+// Lanes of the window at step k (mod 32): (k - j) & 31, j = 0..WM-1.  Lanes
+// outside the true window hold delta = 0, so whole 4-lane blocks are used.
+template <int k, int WM>
+struct WinBlocks {
+  static constexpr bool in(int l) { return ((k - l) & 31) < WM; }
+  static constexpr bool blk(int b) { return in(4 * b) || in(4 * b + 1) || in(4 * b + 2) || in(4 * b + 3); }
+};
+
+template <int k, int WM>
+KAPSM_DEV float window_dot(unsigned dvb, const float (&row)[TC_S], float yz) {
+  using B = WinBlocks<k, WM>;
+  float2 a[4] = {make_float2(yz, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                 make_float2(0.f, 0.f)};
+  int ai = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (B::blk(b)) {
+      const float4 v = lds_f4(dvb + 16 * b);
+      a[ai & 3] = __ffma2_rn(make_float2(v.x, v.y), make_float2(row[4 * b], row[4 * b + 1]), a[ai & 3]);
+      ++ai;
+      a[ai & 3] = __ffma2_rn(make_float2(v.z, v.w), make_float2(row[4 * b + 2], row[4 * b + 3]), a[ai & 3]);
+      ++ai;
+    }
+  }
+  const float2 s = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+  return s.x + s.y;
+}
+template <int k, int WM>
+KAPSM_DEV double window_dot(unsigned dvb, const double (&row)[TC_S], double yz) {
+  using B = WinBlocks<k, WM>;
+  double a[4] = {yz, 0.0, 0.0, 0.0};
+  int ai = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (B::blk(b)) {
+      const double2 v0 = lds_d2(dvb + 32 * b), v1 = lds_d2(dvb + 32 * b + 16);
+      a[ai & 3] = fma(v0.x, row[4 * b], a[ai & 3]); ++ai;
+      a[ai & 3] = fma(v0.y, row[4 * b + 1], a[ai & 3]); ++ai;
+      a[ai & 3] = fma(v1.x, row[4 * b + 2], a[ai & 3]); ++ai;
+      a[ai & 3] = fma(v1.y, row[4 * b + 3], a[ai & 3]); ++ai;
+    }
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+template <typename T> struct WinLoad;
+template <> struct WinLoad<float> { using type = float4; };
+template <> struct WinLoad<double> { using type = double4; };
+
+// the broadcast deltas of the 4-lane blocks that hold window lanes
+template <int k, int WM>
+KAPSM_DEV void window_load(unsigned dvb, float4 (&wl)[8]) {
+  using B = WinBlocks<k, WM>;
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+    if (B::blk(b)) wl[b] = lds_f4(dvb + 16 * b);
+}
+template <int k, int WM>
+KAPSM_DEV void window_load(unsigned dvb, double4 (&wl)[8]) {
+  using B = WinBlocks<k, WM>;
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+    if (B::blk(b)) {
+      const double2 u = lds_d2(dvb + 32 * b), v = lds_d2(dvb + 32 * b + 16);
+      wl[b] = make_double4(u.x, u.y, v.x, v.y);
+    }
+}
+// yz + sum over the window lanes (exactly: row entries of other slots are
+// never read, so a takeover's register writes cannot stall the dot)
+template <int k, int WM>
+KAPSM_DEV float window_fma(const float4 (&wl)[8], const float (&row)[TC_S], float yz) {
+  using B = WinBlocks<k, WM>;
+  float2 a[4] = {make_float2(yz, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                 make_float2(0.f, 0.f)};
+  int ai = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int l = 4 * b + 2 * h;
+      const float dx = h ? wl[b].z : wl[b].x, dy = h ? wl[b].w : wl[b].y;
+      if (B::in(l) && B::in(l + 1)) {
+        a[ai & 3] = __ffma2_rn(make_float2(dx, dy), make_float2(row[l], row[l + 1]), a[ai & 3]);
+        ++ai;
+      } else if (B::in(l)) {
+        a[ai & 3].x = fmaf(dx, row[l], a[ai & 3].x);
+        ++ai;
+      } else if (B::in(l + 1)) {
+        a[ai & 3].y = fmaf(dy, row[l + 1], a[ai & 3].y);
+        ++ai;
+      }
+    }
+  }
+  const float2 s = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+  return s.x + s.y;
+}
+template <int k, int WM>
+KAPSM_DEV double window_fma(const double4 (&wl)[8], const double (&row)[TC_S], double yz) {
+  using B = WinBlocks<k, WM>;
+  double a[4] = {yz, 0.0, 0.0, 0.0};
+  int ai = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int l = 4 * b + e;
+      const double d = e == 0 ? wl[b].x : e == 1 ? wl[b].y : e == 2 ? wl[b].z : wl[b].w;
+      if (B::in(l)) { a[ai & 3] = fma(d, row[l], a[ai & 3]); ++ai; }
+    }
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+// row[l] = buf[(l - c0) & 31], c0 a multiple of 4 (the staged segment's rotation)
+template <int c0>
+KAPSM_DEV void load_row32_rot(unsigned p, float (&r)[TC_S]) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const float4 u = a4[q], w = b4[q];
-    s0 = fmaf(u.x, w.x, s0);
-    s1 = fmaf(u.y, w.y, s1);
-    s2 = fmaf(u.z, w.z, s2);
-    s3 = fmaf(u.w, w.w, s3);
-  }
-  return (s0 + s1) + (s2 + s3);
-}
-KAPSM_DEV double dot32(const double* a, const double* b) {
-  const double2* a2 = reinterpret_cast<const double2*>(a);
-  const double2* b2 = reinterpret_cast<const double2*>(b);
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-  for (int q = 0; q < 16; q += 2) {
-    const double2 u = a2[q], w = b2[q], u2 = a2[q + 1], w2 = b2[q + 1];
-    s0 = fma(u.x, w.x, s0);
-    s1 = fma(u.y, w.y, s1);
-    s2 = fma(u2.x, w2.x, s2);
-    s3 = fma(u2.y, w2.y, s3);
-  }
-  return (s0 + s1) + (s2 + s3);
-}
-
-// the lane's 32-entry Gram row (16-byte aligned smem) into registers
-KAPSM_DEV void load_row32(const float* p, float (&r)[32]) {
-  const float4* p4 = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 v = p4[q];
+    const float4 v = lds_f4(p + 4 * ((4 * q - c0) & (TC_S - 1)));
     r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
   }
 }
-KAPSM_DEV void load_row32(const double* p, double (&r)[32]) {
-  const double2* p2 = reinterpret_cast<const double2*>(p);
+template <int c0>
+KAPSM_DEV void load_row32_rot(unsigned p, double (&r)[TC_S]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const unsigned o = p + 8 * ((4 * q - c0) & (TC_S - 1));
+    const double2 u = lds_d2(o), v = lds_d2(o + 16);
+    r[4 * q] = u.x; r[4 * q + 1] = u.y; r[4 * q + 2] = v.x; r[4 * q + 3] = v.y;
+  }
+}
+
+KAPSM_DEV void load_row32(unsigned p, float (&r)[TC_S]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 v = lds_f4(p + 16 * q);
+    r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+  }
+}
+KAPSM_DEV void load_row32(unsigned p, double (&r)[TC_S]) {
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
-    const double2 v = p2[q];
+    const double2 v = lds_d2(p + 16 * q);
     r[2 * q] = v.x; r[2 * q + 1] = v.y;
   }
 }
-// 32-term dot of a broadcast smem vector (LDS.128) with a register row
-KAPSM_DEV float dot32_reg(const float* a, const float (&r)[32]) {
-  const float4* a4 = reinterpret_cast<const float4*>(a);
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 u = a4[q];
-    s0 = fmaf(u.x, r[4 * q], s0);
-    s1 = fmaf(u.y, r[4 * q + 1], s1);
-    s2 = fmaf(u.z, r[4 * q + 2], s2);
-    s3 = fmaf(u.w, r[4 * q + 3], s3);
-  }
-  return (s0 + s1) + (s2 + s3);
+KAPSM_DEV void warp_sync_full() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
+KAPSM_DEV float recip(float v) {   // MUFU.RCP (FP32 path tolerance is 1e-4)
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
 }
-KAPSM_DEV double dot32_reg(const double* a, const double (&r)[32]) {
-  const double2* a2 = reinterpret_cast<const double2*>(a);
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-  for (int q = 0; q < 16; q += 2) {
-    const double2 u = a2[q], u2 = a2[q + 1];
-    s0 = fma(u.x, r[2 * q], s0);
-    s1 = fma(u.y, r[2 * q + 1], s1);
-    s2 = fma(u2.x, r[2 * q + 2], s2);
-    s3 = fma(u2.y, r[2 * q + 3], s3);
-  }
-  return (s0 + s1) + (s2 + s3);
-}
+KAPSM_DEV double recip(double v) { return 1.0 / v; }
 
-// sum_{i=0..last} c_i row[i] over a warp, with c_i read from the tagged array
-// (value, index) and a mismatch flag instead of a per-element wait.  float:
-// each lane takes 4 consecutive columns per LDS.128 (row) + 2 LDS.128 (tags).
+// Per-lane partial of sum_{i=0..last} c_i row[i], c_i read from the tagged
+// array (value, index); `bad` flags a coefficient that is not yet visible.
+// float: each lane takes 4 consecutive columns per LDS.128 (row) + 2 LDS.128 (tags).
 template <typename T>
-KAPSM_DEV T tagged_dot(const T* row, const typename Tagged<T>::slot_t* ctag, int last, int lane,
-                       bool& bad);
+KAPSM_DEV T tagged_partial(const T* row, const typename Tagged<T>::slot_t* ctag, int last, int lane,
+                           bool& bad);
 template <>
-KAPSM_DEV float tagged_dot<float>(const float* row, const unsigned long long* ctag, int last,
-                                  int lane, bool& bad) {
+KAPSM_DEV float tagged_partial<float>(const float* row, const unsigned long long* ctag, int last,
+                                      int lane, bool& bad) {
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   const int n = last + 1;
   int i = 4 * lane;
+#pragma unroll 4
   for (; i + 3 < n; i += 128) {
     const float4 r = *reinterpret_cast<const float4*>(row + i);
     const uint4 t01 = *reinterpret_cast<const uint4*>(ctag + i);
@@ -157,11 +248,11 @@ KAPSM_DEV float tagged_dot<float>(const float* row, const unsigned long long* ct
     bad |= (int)(w >> 32) != k;
     s0 = fmaf(__uint_as_float((unsigned)(w & 0xffffffffu)), row[k], s0);
   }
-  return warp_sum((s0 + s1) + (s2 + s3));
+  return (s0 + s1) + (s2 + s3);
 }
 template <>
-KAPSM_DEV double tagged_dot<double>(const double* row, const Tagged<double>::slot_t* ctag,
-                                    int last, int lane, bool& bad) {
+KAPSM_DEV double tagged_partial<double>(const double* row, const Tagged<double>::slot_t* ctag,
+                                        int last, int lane, bool& bad) {
   double s0 = 0.0, s1 = 0.0;
   int i = lane;
   for (; i + 32 <= last; i += 64) {
@@ -175,43 +266,100 @@ KAPSM_DEV double tagged_dot<double>(const double* row, const Tagged<double>::slo
     bad |= (int)a.t != i;
     s0 = fma(__longlong_as_double((long long)a.v), row[i], s0);
   }
-  return warp_sum(s0 + s1);
+  return s0 + s1;
+}
+
+// Per-lane partial of sum_{i=0..last} c_i row[i] over plain arrays (the
+// caller has seen c_last published; earlier coefficients were stored first).
+KAPSM_DEV float plain_partial(const float* row, const float* cf, int last, int lane) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const int n = last + 1;
+  int i = 4 * lane;
+#pragma unroll 4
+  for (; i + 3 < n; i += 128) {
+    const float4 r = *reinterpret_cast<const float4*>(row + i);
+    const float4 c = *reinterpret_cast<const float4*>(cf + i);
+    s0 = fmaf(c.x, r.x, s0);
+    s1 = fmaf(c.y, r.y, s1);
+    s2 = fmaf(c.z, r.z, s2);
+    s3 = fmaf(c.w, r.w, s3);
+  }
+  for (int k = i; k < i + 4 && k < n; ++k) s0 = fmaf(cf[k], row[k], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+KAPSM_DEV double plain_partial(const double* row, const double* cf, int last, int lane) {
+  double s0 = 0.0, s1 = 0.0;
+  int i = 2 * lane;
+#pragma unroll 2
+  for (; i + 1 <= last; i += 64) {
+    const double2 r = *reinterpret_cast<const double2*>(row + i);
+    const double2 c = *reinterpret_cast<const double2*>(cf + i);
+    s0 = fma(c.x, r.x, s0);
+    s1 = fma(c.y, r.y, s1);
+  }
+  if (i <= last) s0 = fma(cf[i], row[i], s0);
+  return s0 + s1;
 }
 
 template <typename T>
+KAPSM_DEV T slot_value(const typename Tagged<T>::slot_t& w);
+template <>
+KAPSM_DEV float slot_value<float>(const unsigned long long& w) {
+  return __uint_as_float((unsigned)(w & 0xffffffffu));
+}
+template <>
+KAPSM_DEV double slot_value<double>(const Tagged<double>::slot_t& w) {
+  return __longlong_as_double((long long)w.v);
+}
+
+// Role layout of a CTA with NG groups.
+//   NG = 1 (latency): 7 warps; warp 3 (alone on sub-partition 3) is critical,
+//          warps 0,1,2,4,5,6 are background 0..5.
+//   NG = 4 (throughput): 16 warps; group g = w % 4, role w / 4 (3 = critical).
+template <int NG> struct Roles;
+template <> struct Roles<1> {
+  static constexpr int NB = 6, NBUF = 2, WARPS = 7;
+  static KAPSM_DEV int group(int) { return 0; }
+  static KAPSM_DEV int role(int w) { return w == 3 ? NB : (w < 3 ? w : w - 1); }
+};
+template <> struct Roles<4> {
+  static constexpr int NB = 3, NBUF = 1, WARPS = 16;
+  static KAPSM_DEV int group(int w) { return w & 3; }
+  static KAPSM_DEV int role(int w) { return w >> 2; }
+};
+
+template <typename T, int NG>
 struct GroupSmem {
   // byte offsets of one group's region in dynamic shared memory
-  size_t mbar, pbuf, cring, col, stage, bstage, dbuf, qsm, cfin, fsfin, ring, ctl, total;
-  int npr;   // elements per ring row
+  size_t mbar, dv, snap, stage, sbar, initr, ctag, cfin, fsfin, bsm, qsm, apart, rows, ctl, total;
+  int npr;   // elements per Gram-row buffer
   __host__ __device__ GroupSmem(int W, int Np) {
+    using Slot = typename Tagged<T>::slot_t;
+    constexpr int NB = Roles<NG>::NB, NBUF = Roles<NG>::NBUF;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 15) & ~size_t(15); return r; };
     npr = (Np + 8 + 7) & ~7;
-    mbar = take(TR_BGW * sizeof(unsigned long long));
-    pbuf = take(TR_PBN * sizeof(typename Tagged<T>::slot_t));
-    cring = take((size_t)(Np + 32) * sizeof(typename Tagged<T>::slot_t));
-    col = take((size_t)TR_S * TR_CSTR * sizeof(T));
-    stage = take((size_t)TR_STG * TR_S * sizeof(T));
-    bstage = take((size_t)TR_STG * sizeof(T));
-    dbuf = take(2 * 2 * TR_S * sizeof(T));
-    qsm = take(2 * (size_t)W * sizeof(T));
-    cfin = take((size_t)(Np + 32) * sizeof(T));
-    fsfin = take((size_t)(Np + 32) * sizeof(int));
-    ring = take((size_t)TR_BGW * npr * sizeof(T));      // one Gram-row buffer per bg warp
+    mbar = take(NB * NBUF * sizeof(unsigned long long));
+    dv = take(2 * TC_S * sizeof(T));
+    snap = take((size_t)TC_SNAP * TC_S * sizeof(Slot));
+    o = (o + 127) & ~size_t(127);               // TMA tile destination: 128-byte aligned
+    stage = take((size_t)TC_SRING * TC_BT * TC_S * sizeof(T));
+    sbar = take(TC_SRING * sizeof(unsigned long long));
+    initr = take((size_t)TC_INIT * sizeof(Slot));
+    ctag = take((size_t)(Np + TC_S) * sizeof(Slot));
+    cfin = take((size_t)(Np + TC_S) * sizeof(T));
+    fsfin = take((size_t)(Np + TC_S) * sizeof(int));
+    bsm = take((size_t)(Np + 2 * TC_S) * sizeof(T));
+    qsm = take(2 * (size_t)(W + 1) * sizeof(T));
+    apart = take((size_t)NB * TC_ARING * sizeof(T));
+    rows = take((size_t)NB * NBUF * npr * sizeof(T));
     ctl = take(16 * sizeof(int));
     total = (o + 127) & ~size_t(127);
   }
 };
 
-// NG chain groups per CTA.  Warp w belongs to group w % NG with role w / NG:
-//   NG = 4 (throughput): group g owns sub-partition g (warps g, g+4, g+8, g+12),
-//          its critical warp (role 3) has the highest id there;
-//   NG = 1 (latency): background warps 0-2 on sub-partitions 0-2, the critical
-//          warp alone on sub-partition 3.
-// Either way exactly one CTA runs per SM (registers for NG=4, shared-memory
-// padding for NG=1), so no foreign warp competes with a critical warp.
-template <typename T, int NG, int VAR = 0>
-__global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
+template <typename T, int NG, int WM, bool DBG>
+__global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     apsm_train_kernel(const T* __restrict__ gram, long long ld, long long gram_stride,
                       const T* __restrict__ rx, long long rx_stride,
                       const T* __restrict__ samples, long long samples_stride, int dim,
@@ -220,29 +368,33 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
                       const T* __restrict__ theta0, T* __restrict__ coeff_out,
                       int* __restrict__ fs_out, T* __restrict__ theta_out,
                       int* __restrict__ nact_out, int* __restrict__ status_out,
-                      long long* __restrict__ dbg) {
+                      long long* __restrict__ dbg, const __grid_constant__ CUtensorMap smap) {
   using Slot = typename Tagged<T>::slot_t;
+  using R = Roles<NG>;
+  constexpr int NB = R::NB, NBUF = R::NBUF;
+  constexpr int D = lookahead(WM);            // takeover lookahead (steps)
+  constexpr int FIRST = D;                    // first sample whose init needs coefficients
+  constexpr unsigned TS = sizeof(T), SS = sizeof(Slot);
   extern __shared__ __align__(128) unsigned char smem[];
-  const GroupSmem<T> L(W, Np);
+  const GroupSmem<T, NG> L(W, Np);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = warp % NG;                   // chain group of this warp
-  const int role = warp / NG;                  // 0..BGW-1: background, BGW: critical
+  const int grp = R::group(warp);
+  const int role = R::role(warp);              // 0..NB-1: background, NB: critical
   const int gt = role * 32 + lane;             // thread index inside the group
+  constexpr int GT = (NB + 1) * 32;
   unsigned char* gs = smem + (size_t)grp * L.total;
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(gs + L.mbar);
-  Slot* pbuf = reinterpret_cast<Slot*>(gs + L.pbuf);    // [PBN]   tagged P_m
-  Slot* ctag = reinterpret_cast<Slot*>(gs + L.cring);   // [Np+32] tagged final c_m (+junk)
-  T* col2 = reinterpret_cast<T*>(gs + L.col);           // [S][CSTR]
-  T* stage = reinterpret_cast<T*>(gs + L.stage);        // [STG][S]
-  T* bstage = reinterpret_cast<T*>(gs + L.bstage);      // [STG]
-  T* dbuf = reinterpret_cast<T*>(gs + L.dbuf);          // [2][2S]
-  T* qsm = reinterpret_cast<T*>(gs + L.qsm);            // [W][2]
-  T* cfin = reinterpret_cast<T*>(gs + L.cfin);          // [Np + 32]  (+junk)
-  int* fsfin = reinterpret_cast<int*>(gs + L.fsfin);    // [Np + 32]  (+junk)
-  T* rowbuf = reinterpret_cast<T*>(gs + L.ring);        // [BGW][npr] Gram rows (TMA)
-  int* ctl = reinterpret_cast<int*>(gs + L.ctl);        // [1]=abort [2]=status [3]=nact
+  Slot* snap = reinterpret_cast<Slot*>(gs + L.snap);     // [SNAP][S] tagged c snapshots
+  Slot* initr = reinterpret_cast<Slot*>(gs + L.initr);   // [INIT] tagged init_m
+  Slot* ctag = reinterpret_cast<Slot*>(gs + L.ctag);     // [Np+S] tagged final c_m
+  T* cfin = reinterpret_cast<T*>(gs + L.cfin);           // [Np+S] final c_m (stored before ctag)
+  int* fsfin = reinterpret_cast<int*>(gs + L.fsfin);     // [Np+S] first-activation step
+  T* bsm = reinterpret_cast<T*>(gs + L.bsm);             // [Np+2S] targets (zero padded)
+  T* qsm = reinterpret_cast<T*>(gs + L.qsm);             // [W+1][2] (q_mid, q_last), row W = 0
+  T* rows = reinterpret_cast<T*>(gs + L.rows);           // [NB][NBUF][npr] Gram rows (TMA)
+  int* ctl = reinterpret_cast<int*>(gs + L.ctl);         // [1]=abort [2]=status [3]=nact
   const int group_bar = 1 + grp;
-  const int GT = (TR_BGW + 1) * 32;
+  const int dbgvar = DBG ? (int)dbg[5 * Np] : 0;
 
   for (int task = blockIdx.x * NG + grp; task < F * K; task += gridDim.x * NG) {
     const int fu = task;                        // frame * K + user
@@ -252,156 +404,256 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
     const T* P0 = base0 ? base0 + (long long)fu * Np : nullptr;
 
     // ---------------- per-task group state ----------------
-    for (int i = gt; i < TR_PBN; i += GT) Tagged<T>::store(&pbuf[i], T(0), -1);
-    for (int i = gt; i < Np + 32; i += GT) Tagged<T>::store(&ctag[i], T(0), -1);
-    if (gt == 0) {
-      for (int r = 0; r < TR_BGW; ++r) mbar_init(&mbar[r], 1);
-      mbar_fence_init();
-    }
-    for (int i = gt; i < W; i += GT) {
+    for (int i = gt; i < TC_SNAP * TC_S; i += GT) Tagged<T>::store(&snap[i], T(0), -1);
+    for (int i = gt; i < TC_INIT; i += GT) Tagged<T>::store(&initr[i], T(0), -1);
+    for (int i = gt; i < Np + TC_S; i += GT) { Tagged<T>::store(&ctag[i], T(0), -1); fsfin[i] = -1; }
+    for (int i = gt; i < Np + 2 * TC_S; i += GT) bsm[i] = i < Np ? B[i] : T(0);
+    for (int i = gt; i <= W; i += GT) {
       T qm = T(1) / T(i + 1), ql = qm;
       if (qtab) { qm = qtab[2 * i]; ql = qtab[2 * i + 1]; }
+      if (i == W) { qm = T(0); ql = T(0); }     // steps past the last sample: no update
       qsm[2 * i] = qm;
       qsm[2 * i + 1] = ql;
     }
-    for (int i = gt; i < Np + 32; i += GT) { cfin[i] = T(0); fsfin[i] = -1; }
     if (gt < 16) ctl[gt] = 0;
+    if (gt == 0) {
+      for (int r = 0; r < NB * NBUF; ++r) mbar_init(&mbar[r], 1);
+      unsigned long long* sbar = reinterpret_cast<unsigned long long*>(gs + L.sbar);
+      for (int r = 0; r < TC_SRING; ++r) mbar_init(&sbar[r], 1);
+      mbar_fence_init();
+    }
     named_bar(group_bar, GT);
 
-    if (role == TR_BGW) {
+    if (role == NB) {
       // =========================== CRITICAL WARP ===========================
-      // Lane x owns sample m (m = x mod S) from step m-1 to step m+S-2; d = n-m
-      // (d = -1: enters next, 0 <= d < W: in the window J_n, d = W-1: leaves
-      // after this step, d = S-2: released, slot taken over by m+S).
-      // col2[x][l] = K[sample(l)][m] for every owned sample(l).
+      // Slot x owns sample m = x (mod 32).  Samples 0..D-1 are owned from the
+      // start; after the first step of block j (steps n = 4j .. 4j+3) the
+      // samples that left the window are published, the coefficients are
+      // snapshot, and the batch n+D .. n+D+3 is taken over (it accumulates
+      // from step n+1).  Every shared access goes through 32-bit addresses
+      // from one opaque base.
       const int x = lane;
-      for (int e = x; e < TR_S * TR_S; e += 32) {       // K[0..31][0..31]
-        const int r = e / TR_S, l = e - r * TR_S;
-        T* dst = col2 + r * TR_CSTR + l;
-        if (r < Np && l < Np) cp_async_scalar(dst, G + (long long)r * ld + l);
-        else *dst = T(0);
-      }
-      cp_async_commit();
-      int m = x;
-      T b = (m < Np) ? B[m] : T(0);
-      cp_async_wait<0>();
-      __syncwarp();
-      T Y = (m == 0 && P0) ? P0[0] : T(0), c = T(0);
-      int fs = -1, degen = 0;
-      int d = (m < Np) ? -1 - x : -(1 << 29);
-      const T den0 = (m < Np) ? col2[x * TR_CSTR + x] : T(1);
-      degen |= (m < Np && !(den0 > T(0)));
-      T invden = T(1) / den0;
-      const T* myrow = col2 + x * TR_CSTR;
-      const T qm_ss = qsm[2 * (W - 1)], ql_ss = qsm[2 * (W - 1) + 1];
-      bool aborted = false;
+      const unsigned gbase = opaque_u32(smem_u32(gs));
+      const unsigned dv_s = gbase + (unsigned)L.dv, stage_s = gbase + (unsigned)L.stage;
+      const unsigned snap_s = gbase + (unsigned)L.snap + x * SS;
+      const unsigned initr_s = gbase + (unsigned)L.initr, ctag_s = gbase + (unsigned)L.ctag;
+      const unsigned fsfin_s = gbase + (unsigned)L.fsfin, bsm_s = gbase + (unsigned)L.bsm;
+      const unsigned qsm_s = gbase + (unsigned)L.qsm, cfin_s = gbase + (unsigned)L.cfin;
+      const unsigned sbar_s = gbase + (unsigned)L.sbar;
+      const int Wm1 = W - 1;
+      constexpr int NOWN = D;                   // samples owned from the start
 
-      auto step = [&](const int n, auto steady_tag) {
-        constexpr bool ST = decltype(steady_tag)::value;   // steady state: branches known
-        if (dbg && lane == 0 && fu == 0) dbg[n] = clock64();
-        ++d;
-        // loads independent of this step's chain, issued first
-        T row[TR_S];
-        load_row32(myrow, row);
-        const int me = n + 1;
-        T pv = T(0);
-        const bool pok = Tagged<T>::load(&pbuf[me % TR_PBN], me, pv);
-        int J;
-        T qm, ql;
-        if constexpr (ST) {
-          J = W; qm = qm_ss; ql = ql_ss;
-        } else {
-          J = n + 1 < W ? n + 1 : W;
-          qm = qsm[2 * (J - 1)];
-          ql = qsm[2 * (J - 1) + 1];
-        }
-        // (B) three-case beta on the window (apsm.py:323-335), branch-free
-        const bool inwin = (unsigned)d < (unsigned)J;
-        const T res = Y - b;
-        const T bl = (-res - eps) * invden, bh = (-res + eps) * invden;
-        T beta = res < -eps ? bl : (res > eps ? bh : T(0));
-        beta = inwin ? beta : T(0);
-        const T delta = (d == 0 ? ql : qm) * beta;
-        c += delta;
-        fs = (fs < 0 && beta != T(0)) ? n : fs;
-        // (M) Y_m += sum_l delta_l K[l][m]; the entering sample n+1 instead gets
-        //     its full response sum_l c_l K[l][n+1] + P_{n+1}
-        const bool enter = (d == -1);
-        T* vecs = dbuf + (n & 1) * 2 * TR_S;     // [0,S): delta, [S,2S): c
-        vecs[x] = delta;
-        vecs[TR_S + x] = c;
-        __syncwarp();
-        const T acc = (VAR & 4) ? T(0) : dot32_reg(vecs + (enter ? TR_S : 0), row);
-        if ((ST || me < Np) && !pok) {             // warp-uniform, rare: P not yet published
-          long long spins = 0;
-          while (!Tagged<T>::load(&pbuf[me % TR_PBN], me, pv))
-            if (++spins > TR_SPIN_LIMIT || (spins & 4095) == 0 && ld_volatile(&ctl[1])) {
-              aborted = true;
-              break;
-            }
-          if (dbg && lane == 0 && fu == 0) dbg[Np + n] = spins + 1;
-        }
-        Y = enter ? acc + pv : Y + acc;
-        // (L) sample lo leaves the window after this step: c is final.  Every
-        //     lane stores (non-leaving lanes into junk slots): no branch.
-        {
-          const bool leave = (d == W - 1);
-          const int li = leave ? m : Np + x;
-          cfin[li] = c;
-          fsfin[li] = fs;
-          Tagged<T>::store(&ctag[li], c, leave ? m : -1);
-        }
-        // (P) stage the Gram row of the sample taken over TR_DELTA steps later,
-        //     restricted to the samples owned after that takeover; its target
-        //     is staged by the lane that will own it
-        {
-          const int t = n + TR_DELTA, mt = t + 2;
-          if (!(VAR & 2) && (ST || (mt >= TR_S && mt < Np))) {
-            const int sx = mt - ((mt - x) & (TR_S - 1));      // owned by slot x after takeover
-            T* dst = stage + (t & (TR_STG - 1)) * TR_S + x;
-            if (ST || sx >= 0) cp_async_scalar(dst, G + (long long)mt * ld + sx);
-            if (x == (mt & (TR_S - 1))) cp_async_scalar(bstage + (t & (TR_STG - 1)), B + mt);
-          }
-          cp_async_commit();
-        }
-        // (T) release sample n+2-S, take over sample n+2
-        const int mt = n + 2;
-        if (!(VAR & 2) && (ST || (mt >= TR_S && mt < Np))) {
-          cp_async_wait<TR_DELTA>();               // own copies only: no warp sync needed
-          const int r = mt & (TR_S - 1);
-          const T v = stage[(n & (TR_STG - 1)) * TR_S + x];   // K[mt][sample(x)]
-          const T bn = bstage[n & (TR_STG - 1)];               // valid in lane r
-          col2[x * TR_CSTR + r] = v;
-          col2[r * TR_CSTR + x] = v;
-          const T dnew = __shfl_sync(0xffffffffu, v, r);      // K[mt][mt], warp-uniform
-          degen |= !(dnew > T(0));
-          T inew;
-          if constexpr (sizeof(T) == 4) inew = __fdividef(1.0f, dnew);
-          else inew = T(1) / dnew;
-          const bool take = (x == r);
-          m = take ? mt : m;
-          d = take ? -2 : d;
-          c = take ? T(0) : c;
-          fs = take ? -1 : fs;
-          b = take ? bn : b;
-          invden = take ? inew : invden;
-          __syncwarp();                            // col2 writes before next step's row loads
+      int m = x < NOWN ? x : x - TC_S;          // owned sample
+      bool valid = m >= 0 && m < Np;
+      T row[TC_S];                               // row[l] = K[sample(l)][m]
+#pragma unroll
+      for (int l = 0; l < TC_S; ++l)
+        row[l] = (valid && l < NOWN && l < Np) ? G[(long long)l * ld + m] : T(0);
+      const T den0 = valid ? G[(long long)m * ld + m] : T(1);
+      int degen = valid && !(den0 > T(0));
+      T invden = valid ? T(1) / den0 : T(0);
+      const T b0 = valid ? B[m] : T(0);
+      T bme = b0 - eps, bpe = b0 + eps;        // b -/+ eps of the owned sample
+      T bm = T(0), bp = T(0);                    // ... minus init_m, once entered
+      T Y = T(0), c = T(0);
+      int fs = 0x7fffffff;                       // first step with delta != 0 (min)
+      int mleave = m + Wm1;                      // step after which m leaves the window
+      unsigned cta = ctag_s + (unsigned)m * SS, fsa = fsfin_s + 4u * (unsigned)m;
+      unsigned cfa = cfin_s + (unsigned)m * TS;
+      int nend = Np;                             // set to 0 by the watchdog
+      int nlast = -1;
+
+      // Stage the entering columns of batch j (samples n+D+i, n = 4j) with one
+      // 3-D TMA tile copy: rows n+D .. n+D+3 of this frame's Gram, the 32
+      // columns from n+D-28 (position p <-> slot (p + c0) & 31, c0 =
+      // (n+D+4) & 31, a multiple of 4).  Out-of-range rows/columns are zero
+      // filled by the TMA unit: they only meet invalid slots.
+      const unsigned long long smap_addr = reinterpret_cast<unsigned long long>(&smap);
+      auto stage_issue = [&](int jb) {
+        if (lane == 0) {
+          const int nb = jb * TC_BT;
+          const int slot = jb & (TC_SRING - 1);
+          const unsigned bar = sbar_s + 8u * slot;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"((unsigned)(TC_BT * TC_S * TS))
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(stage_s + slot * TC_BT * TC_S * TS),
+              "l"(smap_addr), "r"(nb + D + TC_BT - TC_S), "r"(nb + D), "r"(f), "r"(bar)
+              : "memory");
         }
       };
+#pragma unroll 1
+      for (int p = 0; p < TC_PF; ++p) stage_issue(p);
 
-      // steady phase: full window, prefetch and takeover always in range
-      const int a0 = TR_S - 2 > W - 1 ? TR_S - 2 : W - 1;
-      const int nB0 = a0 < Np ? a0 : Np;
-      int nB1 = Np - TR_DELTA - 2;
-      if (nB1 < nB0) nB1 = nB0;
-      int n = 0;
-      for (; n < nB0 && !aborted; ++n) step(n, std::false_type{});
-      for (; n < nB1 && !aborted; ++n) step(n, std::true_type{});
-      for (; n < Np && !aborted; ++n) step(n, std::false_type{});
-      // remaining window samples (those that did not leave at the last step)
-      if (!aborted && m < Np && d >= 0 && d < W - 1) {
-        cfin[m] = c;
-        fsfin[m] = fs;
+      // init_m of the samples entering in the next block: issued one step
+      // before it is checked (hidden under the window loads)
+      T iv = T(0);
+      int itag = 0;
+      auto init_load = [&](int e0) {                // the load only; the tag is tested later
+        const int rel = (x - e0) & (TC_S - 1);
+        const int me = e0 + rel;
+        ld_tagged(initr_s + (me & (TC_INIT - 1)) * SS, iv, itag);
+      };
+      auto init_check = [&](int e0) {
+        const int rel = (x - e0) & (TC_S - 1);
+        const bool isent = rel < TC_BT;
+        const int me = e0 + rel;
+        bool iok = !isent || itag == me || me >= Np;
+        if (DBG && (dbgvar & 1)) iok = true;
+        if (!__all_sync(0xffffffffu, iok)) {    // rare: the background warps are late
+          long long spins = 0;
+          for (;;) {
+            bool ok = true;
+            if (isent) ok = ld_tag(initr_s + (me & (TC_INIT - 1)) * SS, me, iv) || me >= Np;
+            if (__all_sync(0xffffffffu, ok)) break;
+            if (++spins > TC_SPIN_LIMIT || ((spins & 4095) == 0 && ld_volatile(&ctl[1]))) {
+              nend = 0; atomicOr(&ctl[2], 4);
+              break;
+            }
+          }
+          if (DBG && lane == 0 && fu == 0 && e0 >= 0) dbg[Np + e0] = spins + 1;
+        }
+        if (isent) { bm = bme - iv; bp = bpe - iv; }
+      };
+      init_load(0);
+      init_check(0);
+
+      T qi, qbm, qbp;
+      // weights of step s (uniform_weights, apsm.py:139-153); s >= Np: zero
+      auto weights = [&](int s) {
+        int idx = s < Wm1 ? s : Wm1;
+        idx = s < Np ? idx : W;
+        T qm, ql;
+        lds_pair<T>(qsm_s + 2 * idx * TS, qm, ql);
+        const int d = s - m;
+        const T qsel = d == 0 ? ql : ((unsigned)d < (unsigned)W ? qm : T(0));
+        qi = qsel * invden;
+        qbm = qi * bm;
+        qbp = qi * bp;
+      };
+      weights(0);
+
+      // one step: the chain (beta -> broadcast -> window dot) with `mid`
+      // issued while the window loads are in flight, then the bookkeeping
+      auto step = [&](const int n, auto kc, const bool fresh, auto&& mid) {
+        constexpr int k = decltype(kc)::value;
+        if (DBG && lane == 0 && fu == 0) dbg[n] = clock64();
+        const T v1 = fma(-qi, Y, qbm), v2 = fma(-qi, Y, qbp);
+        const T delta = fmax(v1, T(0)) + fmin(v2, T(0));   // q/den * shrink(b - f, eps)
+        const unsigned dvb = dv_s + (k & 1) * TC_S * TS;
+        sts(dvb + x * TS, delta);
+        warp_sync_full();
+        typename WinLoad<T>::type wl[8];
+        window_load<k, WM>(dvb, wl);
+        const T yz = fresh ? T(0) : Y;                       // a new slot starts from 0
+        mid();
+        Y = window_fma<k, WM>(wl, row, yz);
+        c += delta;
+        fs = min(fs, delta != T(0) ? n : 0x7fffffff);
+      };
+      auto nothing = [] {};
+
+      auto block = [&](const int n0, auto bc) -> bool {
+        constexpr int k0 = decltype(bc)::value * TC_BT;      // first step of the block mod 32
+        constexpr int c0 = (k0 + D + TC_BT) & (TC_S - 1);     // stage rotation (mult. of 4)
+        const int n = n0 + k0;
+        if (n >= nend) return false;
+        const int jb = n >> 2;
+        auto mark = [&](int idx) {
+          if (DBG && (dbgvar & 4) && lane == 0 && fu == 0) dbg[6 * Np + jb * 8 + idx] = clock64();
+        };
+        const int rel = (x - (k0 + D)) & (TC_S - 1);
+        const bool isnew = rel < TC_BT;                       // slot taken over in this block
+        const int mt = n + D + rel;
+        const int slot = jb & (TC_SRING - 1);
+        const unsigned bar = sbar_s + 8u * slot;
+        const unsigned par = (unsigned)(jb >> 2) & 1u;
+        const unsigned sb = stage_s + slot * TC_BT * TC_S * TS;
+        bool sready = true;
+        // ---- step n (the staged batch is checked under its window loads) ----
+        step(n, ic<(k0 + 0) & 31>{}, false, [&] { sready = mbar_try_wait_s(bar, par); });
+        mark(0);
+        weights(n + 1);
+        // ---- publish samples that left during steps n-3..n (c final) ----
+        if ((unsigned)(n - mleave) < (unsigned)TC_BT && m >= 0) {
+          sts(cfa, c);
+          st_tag(cta, c, m);
+          sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
+        }
+        // ---- snapshot c^(n+1) for the init of the batch taken over now ----
+        st_tag(snap_s + (jb & (TC_SNAP - 1)) * TC_S * SS, c, n + 1);
+        if (!sready) {                                        // rare: staging is late
+          long long spins = 0;
+          while (!mbar_try_wait_s(bar, par))
+            if (++spins > TC_SPIN_LIMIT) { nend = 0; atomicOr(&ctl[2], 8); break; }
+        }
+        mark(1);
+        // ---- step n+1: the new slots start from 0 with their staged columns,
+        //      loaded under the window loads ----
+        T diag = T(0), bt = T(0);
+        step(n + 1, ic<(k0 + 1) & 31>{}, isnew, [&] {
+          const unsigned own = ((x - c0) & (TC_S - 1)) * TS;  // this lane's column position
+#pragma unroll
+          for (int i = 0; i < TC_BT; ++i)
+            row[(k0 + D + i) & (TC_S - 1)] = lds_t<T>(sb + i * TC_S * TS + own);
+          const unsigned mine = sb + (rel & (TC_BT - 1)) * TC_S * TS;
+          if (isnew) load_row32_rot<c0>(mine, row);
+          diag = lds_t<T>(mine + own);
+          bt = lds_t<T>(bsm_s + (unsigned)mt * TS);
+        });
+        mark(2);
+        {
+          const bool v = mt < Np;
+          const T inv = v ? recip(diag) : T(0);
+          degen |= isnew && v && !(diag > T(0));
+          m = isnew ? mt : m;
+          c = isnew ? T(0) : c;
+          fs = isnew ? 0x7fffffff : fs;
+          invden = isnew ? inv : invden;
+          bme = isnew ? bt - eps : bme;
+          bpe = isnew ? bt + eps : bpe;
+          mleave = isnew ? mt + Wm1 : mleave;
+          cta = isnew ? ctag_s + (unsigned)mt * SS : cta;
+          fsa = isnew ? fsfin_s + 4u * (unsigned)mt : fsa;
+          cfa = isnew ? cfin_s + (unsigned)mt * TS : cfa;
+        }
+        weights(n + 2);
+        stage_issue(jb + TC_PF);
+        mark(3);
+        // ---- steps n+2, n+3: init of the next block's entering samples ----
+        step(n + 2, ic<(k0 + 2) & 31>{}, false, [&] { init_load(n + TC_BT); });
+        weights(n + 3);
+        mark(4);
+        step(n + 3, ic<(k0 + 3) & 31>{}, false, [&] { init_check(n + TC_BT); });
+        mark(5);
+        weights(n + TC_BT);
+        nlast = n;                                 // last publication point
+        return true;
+      };
+
+#pragma unroll 1
+      for (int n0 = 0; n0 < nend; n0 += TC_S) {
+        block(n0, ic<0>{}) && block(n0, ic<1>{}) && block(n0, ic<2>{}) && block(n0, ic<3>{}) &&
+            block(n0, ic<4>{}) && block(n0, ic<5>{}) && block(n0, ic<6>{}) &&
+            block(n0, ic<7>{});
+      }
+      // drain the stage ring's outstanding bulk copies before the smem is reused
+#pragma unroll 1
+      for (int p = 0; p < TC_PF; ++p) {
+        const int jb = nlast / TC_BT + 1 + p;
+        const unsigned bar = sbar_s + 8u * (jb & (TC_SRING - 1));
+        long long spins = 0;
+        while (!mbar_try_wait_s(bar, (unsigned)(jb >> 2) & 1u))
+          if (++spins > TC_SPIN_LIMIT) break;
+      }
+      const bool aborted = nend == 0;
+      // samples still in the window after the last step: coefficients final now
+      if (!aborted && nlast >= 0 && m >= 0 && m < Np && mleave > nlast) {
+        sts(cfa, c);
+        st_tag(cta, c, m);
+        sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
       }
       const bool any_degen = __any_sync(0xffffffffu, degen != 0);
       __syncwarp();
@@ -409,58 +661,114 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
         if (any_degen) atomicOr(&ctl[2], KAPSM_TRAIN_DEGENERATE);
         if (aborted) { atomicOr(&ctl[2], KAPSM_TRAIN_STALLED); st_volatile(&ctl[1], 1); }
       }
-    } else {
+    } else if (!(DBG && (dbgvar & 2))) {
       // ========================== BACKGROUND WARPS =========================
-      // Background warp k computes P_m for m = S + k, S + k + BGW, ...:
-      //   P_m = f0(r_m) + sum_{i <= m-S} c_i K[m][i]
-      // one warp-wide dot over Gram row m (coalesced, independent loads) with
-      // the final coefficients from the tagged array, as soon as c_{m-S} is
-      // final (sample m-S leaves the window S-W+1 steps before P_m is needed).
-      for (int mm = 1 + gt; mm < TR_S && mm < Np; mm += TR_BGL)
-        Tagged<T>::store(&pbuf[mm % TR_PBN], P0 ? P0[mm] : T(0), mm);
-      bool stop = false;
-      T* buf = rowbuf + (size_t)role * L.npr;
-      unsigned long long* bar = &mbar[role];
-      // TMA bulk copy of Gram row mm, columns 0..mm-S (16-byte rounded)
-      auto issue_row = [&](int mm) {
-        const unsigned bytes = (unsigned)(((mm - TR_S + 1) * (int)sizeof(T) + 15) & ~15);
+      // Warp j computes init_m for the samples m_t = FIRST + j + t*NB, with
+      // n_m = (m-D) & ~3 the step from which m's slot accumulates:
+      //   init_m = f0(r_m) + sum_{i <= m-Q} cfinal_i K[m][i]                  (A)
+      //          + sum_{m-Q < i < n_m} c_i^(n_m) K[m][i]                       (B)
+      // A only needs coefficients that are final long before m is taken over,
+      // so each warp runs A TC_LAG tasks ahead of B (software pipeline); B
+      // reads final coefficients (i <= n_m - W) or the snapshot taken at the
+      // start of step n_m.  A's Gram row prefix arrives by TMA bulk copy, B's
+      // 64 entries by plain loads issued one A-task ahead.
+      const int j = role;
+      const unsigned gbase = smem_u32(gs);
+      const unsigned snap_s = gbase + (unsigned)L.snap, ctag_s = gbase + (unsigned)L.ctag;
+      const unsigned initr_s = gbase + (unsigned)L.initr;
+      T* apart = reinterpret_cast<T*>(gs + L.apart) + j * TC_ARING;
+      if (j == 0)
+        for (int i = lane; i < FIRST && i < Np; i += 32)
+          st_tag(initr_s + (i & (TC_INIT - 1)) * SS, P0 ? P0[i] : T(0), i);
+      T* bufs = rows + (size_t)j * NBUF * L.npr;
+      unsigned long long* bars = mbar + j * NBUF;
+      auto mtask = [&](int t) { return FIRST + j + t * NB; };
+      // TMA of row m's prefix [0, m-Q] (A's operand)
+      auto issue_row = [&](int t) {
+        const int mt = mtask(t);
+        if (mt >= Np || mt - TC_Q < 0) return;
+        const int slot = t % NBUF;
+        const unsigned bytes = (unsigned)(((mt - TC_Q + 1) * (int)sizeof(T) + 15) & ~15);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, bytes);
-        tma_bulk_g2s(buf, G + (long long)mm * ld, bytes, bar);
+        mbar_expect_tx(&bars[slot], bytes);
+        tma_bulk_g2s(bufs + (size_t)slot * L.npr, G + (long long)mt * ld, bytes, &bars[slot]);
       };
-      unsigned phase = 0;
-      if (lane == 0 && TR_S + role < Np) issue_row(TR_S + role);
-      for (int mm = TR_S + role; mm < Np && !stop; mm += TR_BGW) {
-        const int last = mm - TR_S;                  // dot over i = 0..last
-        // wait for c_last (coefficients are finalised in index order)
-        {
-          T cl;
-          long long spins = 0;
-          while (!Tagged<T>::load(&ctag[last], last, cl))
-            if (((++spins) & 1023) == 0 && (spins > TR_SPIN_LIMIT || ld_volatile(&ctl[1]))) {
-              stop = true;
-              break;
-            }
+      if (lane == 0)
+        for (int t = 0; t < NBUF; ++t) issue_row(t);
+      unsigned phases = 0;
+      bool stop = false;
+      // (A) of task t: partial dot -> apart[t % ARING] (lane 0)
+      auto part_a = [&](int t) {
+        const int mt = mtask(t);
+        if (mt >= Np) return;
+        T a = T(0);
+        const int lastA = mt - TC_Q;
+        if (lastA >= 0) {
+          const int slot = t % NBUF;
+          {
+            long long spins = 0;
+            while (!mbar_try_wait(&bars[slot], (phases >> slot) & 1u))
+              if (++spins > TC_SPIN_LIMIT) { stop = true; atomicOr(&ctl[2], 16); break; }
+            phases ^= 1u << slot;
+          }
+          {
+            T cl;
+            long long spins = 0;
+            while (!stop && !ld_tag(ctag_s + lastA * SS, lastA, cl))
+              if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1])))
+              { stop = true; atomicOr(&ctl[2], 32); }
+          }
+          if (__any_sync(0xffffffffu, stop)) { stop = true; return; }
+          const T* buf = bufs + (size_t)slot * L.npr;
+          a = warp_sum(plain_partial(buf, cfin, lastA, lane));
         }
+        __syncwarp();                                    // every lane is done with buf
+        if (lane == 0) {
+          issue_row(t + NBUF);                           // refill this task's buffer slot
+          apart[t % TC_ARING] = a;
+        }
+      };
+      for (int t = 0; t < TC_LAG; ++t) part_a(t);
+      for (int t = 0; !stop; ++t) {
+        const int mt = mtask(t);
+        if (mt >= Np) break;
+        const int nm = (mt - D) & ~(TC_BT - 1);    // its batch is taken over after step nm
+        // B's Gram entries (2 per lane), loaded ahead of the A task below
+        T kb[2];
+        int ib[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          ib[h] = mt - TC_Q + 1 + lane + 32 * h;
+          kb[h] = (ib[h] >= 0 && ib[h] <= nm) ? G[(long long)mt * ld + ib[h]] : T(0);
+        }
+        const T f0m = P0 ? P0[mt] : T(0);
+        if (DBG && lane == 0 && fu == 0) dbg[3 * Np + mt] = clock64();
+        part_a(t + TC_LAG);
         if (stop) break;
-        {
-          long long spins = 0;
-          while (!mbar_try_wait(bar, phase))
-            if (++spins > TR_SPIN_LIMIT) { stop = true; break; }
-          phase ^= 1u;
+        if (DBG && lane == 0 && fu == 0) dbg[4 * Np + mt] = clock64();
+        T part = T(0);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {                      // (B)
+          const int i = ib[h];
+          if (i >= 0 && i <= nm) {
+            const bool fin = i <= nm - W + 1;            // published before the snapshot
+            const unsigned a = fin ? ctag_s + i * SS
+                                   : snap_s + (((nm >> 2) & (TC_SNAP - 1)) * TC_S + (i & (TC_S - 1))) * SS;
+            const int tag = fin ? i : nm + 1;
+            T cv;
+            long long spins = 0;
+            while (!ld_tag(a, tag, cv))
+              if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1]))) {
+                stop = true; atomicOr(&ctl[2], 64);
+                break;
+              }
+            part = fma(cv, kb[h], part);
+          }
         }
-        if (stop) break;
-        T pm_part;
-        for (;;) {
-          bool bad = false;
-          pm_part = tagged_dot<T>(buf, ctag, last, lane, bad);
-          if (!__any_sync(0xffffffffu, bad)) break;     // a coefficient not yet visible: redo
-        }
-        const T acc0 = pm_part, acc1 = T(0);
-        const T pm = acc0 + acc1;
-        if (lane == 0) Tagged<T>::store(&pbuf[mm % TR_PBN], pm + (P0 ? P0[mm] : T(0)), mm);
-        __syncwarp();                                // every lane is done with buf
-        if (lane == 0 && mm + TR_BGW < Np) issue_row(mm + TR_BGW);
+        if (__any_sync(0xffffffffu, stop)) { stop = true; break; }
+        const T tot = warp_sum(part) + f0m;
+        if (lane == 0) st_tag(initr_s + (mt & (TC_INIT - 1)) * SS, tot + apart[t % TC_ARING], mt);
+        if (DBG && lane == 0 && fu == 0) dbg[2 * Np + mt] = clock64();
       }
       if (stop && lane == 0) { atomicOr(&ctl[2], KAPSM_TRAIN_STALLED); st_volatile(&ctl[1], 1); }
     }
@@ -469,7 +777,7 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
     {
       int na = 0;
       for (int i = gt; i < Np; i += GT) {
-        coeff_out[(long long)fu * Np + i] = cfin[i];
+        coeff_out[(long long)fu * Np + i] = slot_value<T>(ctag[i]);
         const int v = fsfin[i];
         fs_out[(long long)fu * Np + i] = v;
         na += (v >= 0);
@@ -481,33 +789,33 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
     {
       T* th = theta_out + (long long)fu * dim;
       const T* t0 = theta0 ? theta0 + (long long)fu * dim : nullptr;
-      const int nw = TR_BGW + 1;
+      constexpr int nw = NB + 1;
       if (rx) {
         // complex pilots: Theta = theta[:M] + i theta[M:] = w_l sum_p (c_2p - i c_2p+1) x_p
         const int M = dim / 2, n_train = Np / 2;
         const T* X = rx + (long long)f * rx_stride;
-        for (int k = role; k < M; k += nw) {
+        for (int kk = role; kk < M; kk += nw) {
           T tr = T(0), ti = T(0);
           for (int p = lane; p < n_train; p += 32) {
-            const T c1 = cfin[2 * p], c2 = cfin[2 * p + 1];
-            const T xr = X[(long long)p * 2 * M + 2 * k], xi = X[(long long)p * 2 * M + 2 * k + 1];
+            const T c1 = slot_value<T>(ctag[2 * p]), c2 = slot_value<T>(ctag[2 * p + 1]);
+            const T xr = X[(long long)p * 2 * M + 2 * kk], xi = X[(long long)p * 2 * M + 2 * kk + 1];
             tr = fma(c1, xr, fma(c2, xi, tr));
             ti = fma(c1, xi, fma(-c2, xr, ti));
           }
           tr = warp_sum(tr);
           ti = warp_sum(ti);
           if (lane == 0) {
-            th[k] = w_l * tr + (t0 ? t0[k] : T(0));
-            th[M + k] = w_l * ti + (t0 ? t0[M + k] : T(0));
+            th[kk] = w_l * tr + (t0 ? t0[kk] : T(0));
+            th[M + kk] = w_l * ti + (t0 ? t0[M + kk] : T(0));
           }
         }
       } else {
         const T* S = samples + (long long)f * samples_stride;
-        for (int k = role; k < dim; k += nw) {
+        for (int kk = role; kk < dim; kk += nw) {
           T acc = T(0);
-          for (int i = lane; i < Np; i += 32) acc = fma(cfin[i], S[(long long)i * dim + k], acc);
+          for (int i = lane; i < Np; i += 32) acc = fma(slot_value<T>(ctag[i]), S[(long long)i * dim + kk], acc);
           acc = warp_sum(acc);
-          if (lane == 0) th[k] = w_l * acc + (t0 ? t0[k] : T(0));
+          if (lane == 0) th[kk] = w_l * acc + (t0 ? t0[kk] : T(0));
         }
       }
     }
@@ -516,13 +824,18 @@ __global__ void __launch_bounds__(NG * (TR_BGW + 1) * 32, 1)
       status_out[fu] = ctl[2];
       nact_out[fu] = ctl[3];
     }
+    if (gt == 0) {                                 // barriers are re-initialised per task
+      for (int r = 0; r < NB * NBUF; ++r)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mbar[r])) : "memory");
+      unsigned long long* sbar = reinterpret_cast<unsigned long long*>(gs + L.sbar);
+      for (int r = 0; r < TC_SRING; ++r)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sbar[r])) : "memory");
+    }
     named_bar(group_bar, GT);                      // state reused by the next task
   }
 }
 
-static int num_sms_impl();
-static int num_sms() { return num_sms_impl(); }
-static int num_sms_impl() {
+static int num_sms() {
   static int n = 0;
   if (n == 0) {
     int dev = 0;
@@ -533,27 +846,92 @@ static int num_sms_impl() {
   return n;
 }
 
-template <typename T, int NG, int VAR>
-int launch_train(int tasks, size_t group_smem, cudaStream_t s, const T* gram, long long ld,
-                 long long gram_stride, const T* rx, long long rx_stride, const T* samples,
-                 long long samples_stride, int dim, const T* targets, int F, int K, int Np,
-                 int W, double eps, kapsm_kernel_params p, const T* qtab, const T* base0,
-                 const T* theta0, T* coeff, int* first_step, T* theta, int* n_active, int* status,
-                 long long* dbg) {
-  auto kern = apsm_train_kernel<T, NG, VAR>;
-  size_t smem = group_smem * NG;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3-D tile map over the frames' Gram matrices (columns, rows, frames) with a
+// 32 x 4 x 1 box: one TMA copy stages a batch of entering columns.
+template <typename T>
+static int make_stage_map(CUtensorMap* m, const T* gram, int F, int Np, long long ld,
+                          long long gram_stride) {
+  auto enc = tmap_encoder();
+  if (!enc) return KAPSM_ERR_CUDA;
+  const cuuint64_t dims[3] = {(cuuint64_t)Np, (cuuint64_t)Np, (cuuint64_t)(F > 0 ? F : 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(T),
+                                 (cuuint64_t)(gram_stride > 0 ? gram_stride : Np * ld) * sizeof(T)};
+  const cuuint32_t box[3] = {TC_S, TC_BT, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r =
+      enc(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+          const_cast<T*>(gram), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? KAPSM_OK : KAPSM_ERR_INVALID;
+}
+
+template <typename T, int NG, int WM>
+int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long long gram_stride,
+                 const T* rx, long long rx_stride, const T* samples, long long samples_stride,
+                 int dim, const T* targets, int F, int K, int Np, int W, double eps,
+                 kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
+                 int* first_step, T* theta, int* n_active, int* status, long long* dbg,
+                 int var) {
+  auto kern = apsm_train_kernel<T, NG, WM, false>;
+  if constexpr (sizeof(T) == 4 && NG == 1 && WM == 20) {   // clock instrumentation build
+    if (dbg) kern = apsm_train_kernel<T, NG, WM, true>;
+  } else if (dbg) {
+    return KAPSM_ERR_UNSUPPORTED;
+  }
+  const GroupSmem<T, NG> L(W, Np);
+  size_t smem = L.total * NG;
   // NG = 1: pad shared memory so that only one CTA fits per SM
   if (NG == 1 && smem < 120 * 1024) smem = 120 * 1024;
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return KAPSM_ERR_CUDA;
+  CUtensorMap smap;
+  if (int r = make_stage_map(&smap, gram, F, Np, ld, gram_stride)) return r;
   int grid = (tasks + NG - 1) / NG;
   if (grid > num_sms()) grid = num_sms();
-  kern<<<grid, NG * (TR_BGW + 1) * 32, smem, s>>>(
+  if (const char* cap = getenv("KAPSM_GRID_CAP"))
+    if (atoi(cap) > 0 && grid > atoi(cap)) grid = atoi(cap);
+  kern<<<grid, Roles<NG>::WARPS * 32, smem, s>>>(
       gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, targets, F, K, Np, W,
-      (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status, dbg);
+      (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status, dbg,
+      smap);
   return status_from(cudaGetLastError());
+}
+
+template <typename T, int NG>
+int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long long gram_stride,
+                   const T* rx, long long rx_stride, const T* samples, long long samples_stride,
+                   int dim, const T* targets, int F, int K, int Np, int W, double eps,
+                   kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
+                   int* first_step, T* theta, int* n_active, int* status, long long* dbg,
+                   int var) {
+#define KAPSM_LT(WMV)                                                                         \
+  return launch_train<T, NG, WMV>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,    \
+                                  samples_stride, dim, targets, F, K, Np, W, eps, p, qtab,    \
+                                  base0, theta0, coeff, first_step, theta, n_active, status, dbg, var)
+  // the window dot covers the WM newest slots (static per unrolled step)
+  if (W <= 8) KAPSM_LT(8);
+  if (W <= 16) KAPSM_LT(16);
+  if (W <= 20) KAPSM_LT(20);
+  KAPSM_LT(TC_MAX_W);
+#undef KAPSM_LT
 }
 
 template <typename T>
@@ -561,43 +939,42 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
           const T* samples, long long samples_stride, int dim, const T* targets, int F, int K,
           int Np, int W, double eps, kapsm_kernel_params p, const T* qtab, const T* base0,
           const T* theta0, T* coeff, int* first_step, T* theta, int* n_active, int* status,
-          cudaStream_t s, long long* dbg = nullptr, int variant = 0) {
+          cudaStream_t s, long long* dbg = nullptr, int var = 0) {
   if (F < 0 || K < 1 || Np < 1 || dim < 1 || W < 1 || !(eps > 0)) return KAPSM_ERR_INVALID;
   if (F == 0) return KAPSM_OK;
   if (!gram || !targets || !coeff || !first_step || !theta || !n_active || !status)
     return KAPSM_ERR_INVALID;
   if ((rx == nullptr) == (samples == nullptr)) return KAPSM_ERR_INVALID;  // exactly one source
   if (rx && ((Np & 1) || (dim & 1))) return KAPSM_ERR_INVALID;
-  if (W > TR_MAX_W || Np > TR_MAX_NP) return KAPSM_ERR_UNSUPPORTED;
-  // TMA row copies read up to 16 bytes past Np inside each (16-byte aligned) row
-  if (ld < Np + 16 / (long long)sizeof(T) || (ld * (long long)sizeof(T)) % 16 ||
+  if (W > TC_MAX_W || Np > TC_MAX_NP) return KAPSM_ERR_UNSUPPORTED;
+  // TMA copies read whole 16-byte granules and the staged column segments run
+  // up to 11 columns past Np: rows need >= 16 (finite, zero) padding columns
+  if (ld < Np + 16 || (ld * (long long)sizeof(T)) % 16 ||
       (gram_stride * (long long)sizeof(T)) % 16 || ((size_t)gram & 15))
     return KAPSM_ERR_INVALID;
-  GroupSmem<T> L(W, Np);
-  if (L.total > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   const int tasks = F * K;
-  // latency mode (one chain per SM) when the tasks fit on the SMs, else 4 per SM
-  const bool lat = tasks <= num_sms() || L.total * 4 > 227 * 1024;
-#define KAPSM_LT(NGV, V)                                                                     \
-  return launch_train<T, NGV, V>(tasks, L.total, s, gram, ld, gram_stride, rx, rx_stride,    \
-                                 samples, samples_stride, dim, targets, F, K, Np, W, eps, p, \
-                                 qtab, base0, theta0, coeff, first_step, theta, n_active,    \
-                                 status, dbg)
-  if (lat) {
-    switch (variant) {
-      case 4: KAPSM_LT(1, 4);
-      default: KAPSM_LT(1, 0);
-    }
-  }
-  KAPSM_LT(4, 0);
-#undef KAPSM_LT
+  // latency mode (one chain per SM) when the tasks fit on the SMs or 4 groups do not fit
+  // (FP64 is the parity/test precision: latency mode only)
+  static const bool force_lat = getenv("KAPSM_FORCE_LATENCY_MODE") != nullptr;
+  const bool lat = force_lat || sizeof(T) == 8 || tasks <= num_sms() ||
+                   GroupSmem<T, 4>(W, Np).total * 4 > 227 * 1024;
+  if (GroupSmem<T, 1>(W, Np).total > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
+  if (lat)
+    return launch_train_w<T, 1>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
+                                samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
+                                theta0, coeff, first_step, theta, n_active, status, dbg, var);
+  if constexpr (sizeof(T) == 8) return KAPSM_ERR_UNSUPPORTED;
+  else
+    return launch_train_w<T, 4>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
+                              samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
+                              theta0, coeff, first_step, theta, n_active, status, dbg, var);
 }
 
 }  // namespace kapsm
 
-extern "C" int kapsm_max_window(void) { return kapsm::TR_MAX_W; }
+extern "C" int kapsm_max_window(void) { return kapsm::TC_MAX_W; }
 
-extern "C" int kapsm_max_samples(void) { return kapsm::TR_MAX_NP; }
+extern "C" int kapsm_max_samples(void) { return kapsm::TC_MAX_NP; }
 
 #define KAPSM_TRAIN_ENTRY(NAME, T)                                                             \
   extern "C" int NAME(const T* gram, long long ld, long long gram_stride, const T* rx,         \

@@ -27,9 +27,10 @@ __all__ = ["FramePipeline", "host_frames"]
 
 
 def _ld(n: int) -> int:
-    """Gram row stride: 16-byte aligned rows with >= 16 bytes of padding past the
-    last sample (the trainer's TMA row copies round up to 16 bytes)."""
-    return (n + 8 + 31) // 32 * 32
+    """Gram row stride: 128-byte aligned rows with >= 16 zero columns past the
+    last sample (the trainer's TMA copies read whole 16-byte granules and the
+    staged column segments run up to 11 columns past the last sample)."""
+    return (n + 16 + 31) // 32 * 32
 
 
 class FramePipeline:
