@@ -13,6 +13,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libkapsm_b200.so")
+# developer knob (kernel experiments): load another build of the same C ABI
+LIB_PATH = os.environ.get("KAPSM_LIB_PATH", LIB_PATH)
 
 KAPSM_OK = 0
 KAPSM_ERR_INVALID = 1

@@ -224,7 +224,7 @@ def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,
             f"window {cfg.window} / {N} realified samples exceed this build's trainer limits "
             f"(window <= {lib.kapsm_max_window()}, samples <= {lib.kapsm_max_samples()})")
     ld = _ld(N)
-    gram = dv.zeros((N, ld), prec)
+    gram = dv.zeros((N + 32, ld), prec)        # + the trainer's zero tail rows
     if rx_pilots is not None:
         _lib.check(dv.fn("kapsm_pilot_gram", prec)(dv.ptr(rxd), N * M, 1, T, M, kp, dv.ptr(gram),
                                                    ld, N * ld, st), "pilot_gram")

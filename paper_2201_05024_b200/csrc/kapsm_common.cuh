@@ -265,3 +265,36 @@ KAPSM_DEV void ld_tagged(unsigned a, double& v, int& tag) {
   tag = (int)t;
 }
 }  // namespace kapsm
+
+namespace kapsm {
+// loads of shared data that is immutable while they run (no volatile, no
+// memory clobber: the compiler may hoist and schedule them freely)
+KAPSM_DEV float lds_nv(unsigned a, float) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+KAPSM_DEV double lds_nv(unsigned a, double) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+KAPSM_DEV void lds_nv_pair(unsigned a, float& x, float& y) {
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+}
+KAPSM_DEV void lds_nv_pair(unsigned a, double& x, double& y) {
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+// warp-wide vote without the compiler's divergence guard (callers are converged)
+KAPSM_DEV bool vote_all(bool p) {
+  unsigned r;
+  asm volatile(
+      "{\n\t.reg .pred a, b;\n\t"
+      "setp.ne.u32 a, %1, 0;\n\t"
+      "vote.sync.all.pred b, a, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, b;\n\t}"
+      : "=r"(r)
+      : "r"((unsigned)p));
+  return r != 0;
+}
+}  // namespace kapsm

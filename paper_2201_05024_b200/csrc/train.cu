@@ -36,12 +36,16 @@
 // only warp on its SM sub-partition, six background warps on the other three.
 // Throughput mode (NG = 4): group g lives on sub-partition g, its critical
 // warp has the highest warp id there (the issue arbiter favours it).
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include "kapsm_common.cuh"
+
+// KAPSM_FEAT (experiments only): bits that compile parts of the critical warp
+// out of the instrumentation kernel, to time them; 0 in every product build.
+#ifndef KAPSM_FEAT
+#define KAPSM_FEAT 0
+#endif
 
 namespace kapsm {
 
@@ -50,6 +54,7 @@ constexpr int TC_BT = 4;                    // batch: takeover / entry / publica
 constexpr int TC_MAX_W = 24;                // lookahead D >= 4 with D + W <= 29
 constexpr int TC_PF = 2;                    // column prefetch distance (batches)
 constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2 > PF)
+constexpr int TC_TAIL_ROWS = 32;            // zero Gram rows required past the last frame
 constexpr int TC_SNAP = 8;                  // coefficient snapshots (ring of batches)
 constexpr int TC_INIT = 64;                 // init values (ring, pow2)
 constexpr int TC_Q = 64;                    // init part A covers i <= m - Q
@@ -111,74 +116,39 @@ KAPSM_DEV double window_dot(unsigned dvb, const double (&row)[TC_S], double yz) 
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
 
+// The broadcast deltas are stored rotated: lane x writes position
+// (x - k - 1) & 31 at step k, so the window lanes (k - j) & 31, j < WM,
+// always occupy positions 32-WM .. 31 (whole 16-byte blocks for WM % 4 == 0),
+// and position p belongs to lane (p + k + 1) & 31 (static per unrolled step).
 template <typename T> struct WinLoad;
 template <> struct WinLoad<float> { using type = float4; };
 template <> struct WinLoad<double> { using type = double4; };
 
-// the broadcast deltas of the 4-lane blocks that hold window lanes
-template <int k, int WM>
+template <int WM>
 KAPSM_DEV void window_load(unsigned dvb, float4 (&wl)[8]) {
-  using B = WinBlocks<k, WM>;
 #pragma unroll
-  for (int b = 0; b < 8; ++b)
-    if (B::blk(b)) wl[b] = lds_f4(dvb + 16 * b);
+  for (int b = (TC_S - WM) / 4; b < 8; ++b) wl[b] = lds_f4(dvb + 16 * b);
 }
-template <int k, int WM>
+template <int WM>
 KAPSM_DEV void window_load(unsigned dvb, double4 (&wl)[8]) {
-  using B = WinBlocks<k, WM>;
 #pragma unroll
-  for (int b = 0; b < 8; ++b)
-    if (B::blk(b)) {
-      const double2 u = lds_d2(dvb + 32 * b), v = lds_d2(dvb + 32 * b + 16);
-      wl[b] = make_double4(u.x, u.y, v.x, v.y);
-    }
-}
-// yz + sum over the window lanes (exactly: row entries of other slots are
-// never read, so a takeover's register writes cannot stall the dot)
-template <int k, int WM>
-KAPSM_DEV float window_fma(const float4 (&wl)[8], const float (&row)[TC_S], float yz) {
-  using B = WinBlocks<k, WM>;
-  float2 a[4] = {make_float2(yz, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                 make_float2(0.f, 0.f)};
-  int ai = 0;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int l = 4 * b + 2 * h;
-      const float dx = h ? wl[b].z : wl[b].x, dy = h ? wl[b].w : wl[b].y;
-      if (B::in(l) && B::in(l + 1)) {
-        a[ai & 3] = __ffma2_rn(make_float2(dx, dy), make_float2(row[l], row[l + 1]), a[ai & 3]);
-        ++ai;
-      } else if (B::in(l)) {
-        a[ai & 3].x = fmaf(dx, row[l], a[ai & 3].x);
-        ++ai;
-      } else if (B::in(l + 1)) {
-        a[ai & 3].y = fmaf(dy, row[l + 1], a[ai & 3].y);
-        ++ai;
-      }
-    }
+  for (int b = (TC_S - WM) / 4; b < 8; ++b) {
+    const double2 u = lds_d2(dvb + 32 * b), v = lds_d2(dvb + 32 * b + 16);
+    wl[b] = make_double4(u.x, u.y, v.x, v.y);
   }
-  const float2 s = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
-  return s.x + s.y;
 }
-template <int k, int WM>
-KAPSM_DEV double window_fma(const double4 (&wl)[8], const double (&row)[TC_S], double yz) {
-  using B = WinBlocks<k, WM>;
-  double a[4] = {yz, 0.0, 0.0, 0.0};
-  int ai = 0;
+KAPSM_DEV float w4(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+KAPSM_DEV double w4(const double4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+// yz + sum over the window positions of delta * row[lane(position)]; scalar
+// FMAs in 4 accumulators (lower latency than FFMA2 on this chain)
+template <int k, int WM, typename T>
+KAPSM_DEV T window_fma(const typename WinLoad<T>::type (&wl)[8], const T (&row)[TC_S], T yz) {
+  T a[4] = {yz, T(0), T(0), T(0)};
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int l = 4 * b + e;
-      const double d = e == 0 ? wl[b].x : e == 1 ? wl[b].y : e == 2 ? wl[b].z : wl[b].w;
-      if (B::in(l)) { a[ai & 3] = fma(d, row[l], a[ai & 3]); ++ai; }
-    }
-  }
+  for (int p = TC_S - WM; p < TC_S; ++p)
+    a[p & 3] = fma(w4(wl[p >> 2], p & 3), row[(p + k + 1) & (TC_S - 1)], a[p & 3]);
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
-
 // row[l] = buf[(l - c0) & 31], c0 a multiple of 4 (the staged segment's rotation)
 template <int c0>
 KAPSM_DEV void load_row32_rot(unsigned p, float (&r)[TC_S]) {
@@ -331,7 +301,7 @@ template <> struct Roles<4> {
 template <typename T, int NG>
 struct GroupSmem {
   // byte offsets of one group's region in dynamic shared memory
-  size_t mbar, dv, snap, stage, sbar, initr, ctag, cfin, fsfin, bsm, qsm, apart, rows, ctl, total;
+  size_t mbar, dv, snap, stage, initr, ctag, cfin, fsfin, bsm, qsm, apart, rows, ctl, total;
   int npr;   // elements per Gram-row buffer
   __host__ __device__ GroupSmem(int W, int Np) {
     using Slot = typename Tagged<T>::slot_t;
@@ -342,9 +312,7 @@ struct GroupSmem {
     mbar = take(NB * NBUF * sizeof(unsigned long long));
     dv = take(2 * TC_S * sizeof(T));
     snap = take((size_t)TC_SNAP * TC_S * sizeof(Slot));
-    o = (o + 127) & ~size_t(127);               // TMA tile destination: 128-byte aligned
     stage = take((size_t)TC_SRING * TC_BT * TC_S * sizeof(T));
-    sbar = take(TC_SRING * sizeof(unsigned long long));
     initr = take((size_t)TC_INIT * sizeof(Slot));
     ctag = take((size_t)(Np + TC_S) * sizeof(Slot));
     cfin = take((size_t)(Np + TC_S) * sizeof(T));
@@ -358,6 +326,24 @@ struct GroupSmem {
   }
 };
 
+// slow path of the entry check (the background warps are late): out of line,
+// so the hot loop carries only a predicated call
+template <typename T>
+__device__ __noinline__ void init_spin(unsigned a, bool isent, int me, int Np, T* iv, int* ctl,
+                                       int* nend) {
+  long long spins = 0;
+  for (;;) {
+    bool ok = true;
+    if (isent) ok = ld_tag(a, me, *iv) || me >= Np;
+    if (vote_all(ok)) break;
+    if (++spins > TC_SPIN_LIMIT || ((spins & 4095) == 0 && ld_volatile(&ctl[1]))) {
+      *nend = 0;
+      atomicOr(&ctl[2], 4);
+      break;
+    }
+  }
+}
+
 template <typename T, int NG, int WM, bool DBG>
 __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     apsm_train_kernel(const T* __restrict__ gram, long long ld, long long gram_stride,
@@ -368,11 +354,12 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
                       const T* __restrict__ theta0, T* __restrict__ coeff_out,
                       int* __restrict__ fs_out, T* __restrict__ theta_out,
                       int* __restrict__ nact_out, int* __restrict__ status_out,
-                      long long* __restrict__ dbg, const __grid_constant__ CUtensorMap smap) {
+                      long long* __restrict__ dbg) {
   using Slot = typename Tagged<T>::slot_t;
   using R = Roles<NG>;
   constexpr int NB = R::NB, NBUF = R::NBUF;
   constexpr int D = lookahead(WM);            // takeover lookahead (steps)
+  constexpr int FEAT = KAPSM_FEAT;            // experiments only: parts compiled out
   constexpr int FIRST = D;                    // first sample whose init needs coefficients
   constexpr unsigned TS = sizeof(T), SS = sizeof(Slot);
   extern __shared__ __align__(128) unsigned char smem[];
@@ -418,8 +405,6 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     if (gt < 16) ctl[gt] = 0;
     if (gt == 0) {
       for (int r = 0; r < NB * NBUF; ++r) mbar_init(&mbar[r], 1);
-      unsigned long long* sbar = reinterpret_cast<unsigned long long*>(gs + L.sbar);
-      for (int r = 0; r < TC_SRING; ++r) mbar_init(&sbar[r], 1);
       mbar_fence_init();
     }
     named_bar(group_bar, GT);
@@ -439,7 +424,6 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       const unsigned initr_s = gbase + (unsigned)L.initr, ctag_s = gbase + (unsigned)L.ctag;
       const unsigned fsfin_s = gbase + (unsigned)L.fsfin, bsm_s = gbase + (unsigned)L.bsm;
       const unsigned qsm_s = gbase + (unsigned)L.qsm, cfin_s = gbase + (unsigned)L.cfin;
-      const unsigned sbar_s = gbase + (unsigned)L.sbar;
       const int Wm1 = W - 1;
       constexpr int NOWN = D;                   // samples owned from the start
 
@@ -463,26 +447,19 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       int nend = Np;                             // set to 0 by the watchdog
       int nlast = -1;
 
-      // Stage the entering columns of batch j (samples n+D+i, n = 4j) with one
-      // 3-D TMA tile copy: rows n+D .. n+D+3 of this frame's Gram, the 32
-      // columns from n+D-28 (position p <-> slot (p + c0) & 31, c0 =
-      // (n+D+4) & 31, a multiple of 4).  Out-of-range rows/columns are zero
-      // filled by the TMA unit: they only meet invalid slots.
-      const unsigned long long smap_addr = reinterpret_cast<unsigned long long>(&smap);
+      // Stage the entering columns of batch j (samples n+D+i, n = 4j): lane x
+      // copies K[n+D+i][sx] (cp.async, 4 bytes each) with sx = x's sample after
+      // the batch, into stage[slot][i][x].  Reads before a row start or past
+      // the last sample land in finite Gram entries or the workspace's zero
+      // tail rows: they only meet invalid slots.
       auto stage_issue = [&](int jb) {
-        if (lane == 0) {
-          const int nb = jb * TC_BT;
-          const int slot = jb & (TC_SRING - 1);
-          const unsigned bar = sbar_s + 8u * slot;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                       "r"((unsigned)(TC_BT * TC_S * TS))
-                       : "memory");
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(stage_s + slot * TC_BT * TC_S * TS),
-              "l"(smap_addr), "r"(nb + D + TC_BT - TC_S), "r"(nb + D), "r"(f), "r"(bar)
-              : "memory");
-        }
+        const int mb = jb * TC_BT + D + TC_BT - 1;
+        const int sx = mb - ((mb - x) & (TC_S - 1));
+        const T* src = G + ((long long)(mb - (TC_BT - 1)) * ld + sx);
+        const unsigned dst = stage_s + ((jb & (TC_SRING - 1)) * TC_BT * TC_S + x) * TS;
+#pragma unroll
+        for (int i = 0; i < TC_BT; ++i) cp_async_s(dst + i * TC_S * TS, src + i * ld);
+        cp_async_commit();
       };
 #pragma unroll 1
       for (int p = 0; p < TC_PF; ++p) stage_issue(p);
@@ -501,19 +478,10 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         const bool isent = rel < TC_BT;
         const int me = e0 + rel;
         bool iok = !isent || itag == me || me >= Np;
-        if (DBG && (dbgvar & 1)) iok = true;
-        if (!__all_sync(0xffffffffu, iok)) {    // rare: the background warps are late
-          long long spins = 0;
-          for (;;) {
-            bool ok = true;
-            if (isent) ok = ld_tag(initr_s + (me & (TC_INIT - 1)) * SS, me, iv) || me >= Np;
-            if (__all_sync(0xffffffffu, ok)) break;
-            if (++spins > TC_SPIN_LIMIT || ((spins & 4095) == 0 && ld_volatile(&ctl[1]))) {
-              nend = 0; atomicOr(&ctl[2], 4);
-              break;
-            }
-          }
-          if (DBG && lane == 0 && fu == 0 && e0 >= 0) dbg[Np + e0] = spins + 1;
+        if ((DBG && (dbgvar & 1)) || (FEAT & 256)) iok = true;
+        if (!vote_all(iok)) {                   // rare: the background warps are late
+          init_spin<T>(initr_s + (me & (TC_INIT - 1)) * SS, isent, me, Np, &iv, ctl, &nend);
+          if (DBG && lane == 0 && fu == 0 && e0 >= 0) dbg[Np + e0] = 1;
         }
         if (isent) { bm = bme - iv; bp = bpe - iv; }
       };
@@ -521,43 +489,53 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       init_check(0);
 
       T qi, qbm, qbp;
-      // weights of step s (uniform_weights, apsm.py:139-153); s >= Np: zero
-      auto weights = [&](int s) {
+      // weights of step s (uniform_weights, apsm.py:139-153): (qm, ql) = the
+      // table row min(s, W-1), or zeros past the last sample
+      auto qload = [&](int s, T& qm, T& ql) {
         int idx = s < Wm1 ? s : Wm1;
         idx = s < Np ? idx : W;
-        T qm, ql;
-        lds_pair<T>(qsm_s + 2 * idx * TS, qm, ql);
+        lds_nv_pair(qsm_s + 2 * idx * TS, qm, ql);       // immutable table: hoistable
+      };
+      auto weights = [&](int s, T qm, T ql) {
         const int d = s - m;
         const T qsel = d == 0 ? ql : ((unsigned)d < (unsigned)W ? qm : T(0));
         qi = qsel * invden;
         qbm = qi * bm;
         qbp = qi * bp;
       };
-      weights(0);
+      {
+        T qm, ql;
+        qload(0, qm, ql);
+        weights(0, qm, ql);
+      }
+      T qcm[TC_BT], qcl[TC_BT];                  // table rows of the current block's steps 1..4
+#pragma unroll
+      for (int i = 0; i < TC_BT; ++i) qload(1 + i, qcm[i], qcl[i]);
 
       // one step: the chain (beta -> broadcast -> window dot) with `mid`
       // issued while the window loads are in flight, then the bookkeeping
       auto step = [&](const int n, auto kc, const bool fresh, auto&& mid) {
         constexpr int k = decltype(kc)::value;
-        if (DBG && lane == 0 && fu == 0) dbg[n] = clock64();
+        if (DBG && !(dbgvar & 8) && lane == 0 && fu == 0) dbg[n] = clock64();
         const T v1 = fma(-qi, Y, qbm), v2 = fma(-qi, Y, qbp);
         const T delta = fmax(v1, T(0)) + fmin(v2, T(0));   // q/den * shrink(b - f, eps)
         const unsigned dvb = dv_s + (k & 1) * TC_S * TS;
-        sts(dvb + x * TS, delta);
+        sts(dvb + ((x + (TC_S - 1 - k)) & (TC_S - 1)) * TS, delta);   // rotated position
         warp_sync_full();
         typename WinLoad<T>::type wl[8];
-        window_load<k, WM>(dvb, wl);
+        window_load<WM>(dvb, wl);
         const T yz = fresh ? T(0) : Y;                       // a new slot starts from 0
         mid();
-        Y = window_fma<k, WM>(wl, row, yz);
-        c += delta;
-        fs = min(fs, delta != T(0) ? n : 0x7fffffff);
+        Y = window_fma<k, WM, T>(wl, row, yz);
+        if (!(FEAT & 64)) {
+          c += delta;
+          fs = min(fs, delta != T(0) ? n : 0x7fffffff);
+        }
       };
       auto nothing = [] {};
 
       auto block = [&](const int n0, auto bc) -> bool {
         constexpr int k0 = decltype(bc)::value * TC_BT;      // first step of the block mod 32
-        constexpr int c0 = (k0 + D + TC_BT) & (TC_S - 1);     // stage rotation (mult. of 4)
         const int n = n0 + k0;
         if (n >= nend) return false;
         const int jb = n >> 2;
@@ -567,44 +545,48 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         const int rel = (x - (k0 + D)) & (TC_S - 1);
         const bool isnew = rel < TC_BT;                       // slot taken over in this block
         const int mt = n + D + rel;
-        const int slot = jb & (TC_SRING - 1);
-        const unsigned bar = sbar_s + 8u * slot;
-        const unsigned par = (unsigned)(jb >> 2) & 1u;
-        const unsigned sb = stage_s + slot * TC_BT * TC_S * TS;
-        bool sready = true;
-        // ---- step n (the staged batch is checked under its window loads) ----
-        step(n, ic<(k0 + 0) & 31>{}, false, [&] { sready = mbar_try_wait_s(bar, par); });
+        const unsigned sb = stage_s + (jb & (TC_SRING - 1)) * TC_BT * TC_S * TS;
+        // ---- step n; under its window loads: next step's weights (each
+        //      step's weights are formed under the previous step's loads, off
+        //      the chain) and this block's staged batch ----
+        step(n, ic<(k0 + 0) & 31>{}, false, [&] {
+          if (!(FEAT & 32)) weights(n + 1, qcm[0], qcl[0]);
+          if (!(FEAT & 8)) cp_async_wait<TC_PF - 1>();
+        });
         mark(0);
-        weights(n + 1);
-        // ---- publish samples that left during steps n-3..n (c final) ----
-        if ((unsigned)(n - mleave) < (unsigned)TC_BT && m >= 0) {
-          sts(cfa, c);
-          st_tag(cta, c, m);
-          sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
+        if (!(FEAT & 1)) {
+          // ---- publish samples that left during steps n-3..n (c final) ----
+          if ((unsigned)(n - mleave) < (unsigned)TC_BT && m >= 0) {
+            sts(cfa, c);
+            st_tag(cta, c, m);
+            sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
+          }
+          // ---- snapshot c^(n+1) for the init of the batch taken over now ----
+          st_tag(snap_s + (jb & (TC_SNAP - 1)) * TC_S * SS, c, n + 1);
         }
-        // ---- snapshot c^(n+1) for the init of the batch taken over now ----
-        st_tag(snap_s + (jb & (TC_SNAP - 1)) * TC_S * SS, c, n + 1);
-        if (!sready) {                                        // rare: staging is late
-          long long spins = 0;
-          while (!mbar_try_wait_s(bar, par))
-            if (++spins > TC_SPIN_LIMIT) { nend = 0; atomicOr(&ctl[2], 8); break; }
-        }
+        warp_sync_full();                                     // staged batch visible to all
         mark(1);
-        // ---- step n+1: the new slots start from 0 with their staged columns,
-        //      loaded under the window loads ----
+        // ---- step n+1: the new slots start from 0 with their staged columns
+        //      (loaded under the window loads); init of the next block's
+        //      entering samples is loaded too ----
         T diag = T(0), bt = T(0);
         step(n + 1, ic<(k0 + 1) & 31>{}, isnew, [&] {
-          const unsigned own = ((x - c0) & (TC_S - 1)) * TS;  // this lane's column position
+          if (!(FEAT & 2)) {
 #pragma unroll
-          for (int i = 0; i < TC_BT; ++i)
-            row[(k0 + D + i) & (TC_S - 1)] = lds_t<T>(sb + i * TC_S * TS + own);
-          const unsigned mine = sb + (rel & (TC_BT - 1)) * TC_S * TS;
-          if (isnew) load_row32_rot<c0>(mine, row);
-          diag = lds_t<T>(mine + own);
-          bt = lds_t<T>(bsm_s + (unsigned)mt * TS);
+            for (int i = 0; i < TC_BT; ++i)
+              row[(k0 + D + i) & (TC_S - 1)] = lds_t<T>(sb + (i * TC_S + x) * TS);
+            if (isnew) load_row32(sb + (rel & (TC_BT - 1)) * TC_S * TS, row);
+          }
+          if (!(FEAT & 4)) {
+            diag = lds_t<T>(sb + ((rel & (TC_BT - 1)) * TC_S + x) * TS);
+            bt = lds_nv(bsm_s + (unsigned)mt * TS, T(0));
+          }
+          if (!(FEAT & 16)) init_load(n + TC_BT);
+          // (zero for the taken-over slots with either their old or new state)
+          if (!(FEAT & 32)) weights(n + 2, qcm[1], qcl[1]);
         });
         mark(2);
-        {
+        if (!(FEAT & 4)) {
           const bool v = mt < Np;
           const T inv = v ? recip(diag) : T(0);
           degen |= isnew && v && !(diag > T(0));
@@ -619,16 +601,23 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
           fsa = isnew ? fsfin_s + 4u * (unsigned)mt : fsa;
           cfa = isnew ? cfin_s + (unsigned)mt * TS : cfa;
         }
-        weights(n + 2);
-        stage_issue(jb + TC_PF);
         mark(3);
-        // ---- steps n+2, n+3: init of the next block's entering samples ----
-        step(n + 2, ic<(k0 + 2) & 31>{}, false, [&] { init_load(n + TC_BT); });
-        weights(n + 3);
+        // ---- step n+2: entry check of the next block's samples, staging of a
+        //      later batch ----
+        step(n + 2, ic<(k0 + 2) & 31>{}, false, [&] {
+          if (!(FEAT & 32)) weights(n + 3, qcm[2], qcl[2]);
+          if (!(FEAT & 16)) init_check(n + TC_BT);
+        });
+        if (!(FEAT & 8)) stage_issue(jb + TC_PF);
         mark(4);
-        step(n + 3, ic<(k0 + 3) & 31>{}, false, [&] { init_check(n + TC_BT); });
+        step(n + 3, ic<(k0 + 3) & 31>{}, false, [&] {
+          if (!(FEAT & 32)) {
+            weights(n + TC_BT, qcm[3], qcl[3]);
+#pragma unroll
+            for (int i = 0; i < TC_BT; ++i) qload(n + TC_BT + 1 + i, qcm[i], qcl[i]);
+          }
+        });
         mark(5);
-        weights(n + TC_BT);
         nlast = n;                                 // last publication point
         return true;
       };
@@ -639,15 +628,7 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
             block(n0, ic<4>{}) && block(n0, ic<5>{}) && block(n0, ic<6>{}) &&
             block(n0, ic<7>{});
       }
-      // drain the stage ring's outstanding bulk copies before the smem is reused
-#pragma unroll 1
-      for (int p = 0; p < TC_PF; ++p) {
-        const int jb = nlast / TC_BT + 1 + p;
-        const unsigned bar = sbar_s + 8u * (jb & (TC_SRING - 1));
-        long long spins = 0;
-        while (!mbar_try_wait_s(bar, (unsigned)(jb >> 2) & 1u))
-          if (++spins > TC_SPIN_LIMIT) break;
-      }
+      cp_async_wait<0>();                       // outstanding staged batches
       const bool aborted = nend == 0;
       // samples still in the window after the last step: coefficients final now
       if (!aborted && nlast >= 0 && m >= 0 && m < Np && mleave > nlast) {
@@ -661,7 +642,7 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         if (any_degen) atomicOr(&ctl[2], KAPSM_TRAIN_DEGENERATE);
         if (aborted) { atomicOr(&ctl[2], KAPSM_TRAIN_STALLED); st_volatile(&ctl[1], 1); }
       }
-    } else if (!(DBG && (dbgvar & 2))) {
+    } else if (!(DBG && (dbgvar & 2)) && !(FEAT & 128)) {
       // ========================== BACKGROUND WARPS =========================
       // Warp j computes init_m for the samples m_t = FIRST + j + t*NB, with
       // n_m = (m-D) & ~3 the step from which m's slot accumulates:
@@ -827,9 +808,6 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     if (gt == 0) {                                 // barriers are re-initialised per task
       for (int r = 0; r < NB * NBUF; ++r)
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mbar[r])) : "memory");
-      unsigned long long* sbar = reinterpret_cast<unsigned long long*>(gs + L.sbar);
-      for (int r = 0; r < TC_SRING; ++r)
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sbar[r])) : "memory");
     }
     named_bar(group_bar, GT);                      // state reused by the next task
   }
@@ -844,41 +822,6 @@ static int num_sms() {
       n = 148;
   }
   return n;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  });
-  return fn;
-}
-
-// 3-D tile map over the frames' Gram matrices (columns, rows, frames) with a
-// 32 x 4 x 1 box: one TMA copy stages a batch of entering columns.
-template <typename T>
-static int make_stage_map(CUtensorMap* m, const T* gram, int F, int Np, long long ld,
-                          long long gram_stride) {
-  auto enc = tmap_encoder();
-  if (!enc) return KAPSM_ERR_CUDA;
-  const cuuint64_t dims[3] = {(cuuint64_t)Np, (cuuint64_t)Np, (cuuint64_t)(F > 0 ? F : 1)};
-  const cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(T),
-                                 (cuuint64_t)(gram_stride > 0 ? gram_stride : Np * ld) * sizeof(T)};
-  const cuuint32_t box[3] = {TC_S, TC_BT, 1};
-  const cuuint32_t es[3] = {1, 1, 1};
-  const CUresult r =
-      enc(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
-          const_cast<T*>(gram), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? KAPSM_OK : KAPSM_ERR_INVALID;
 }
 
 template <typename T, int NG, int WM>
@@ -902,16 +845,13 @@ int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long lo
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return KAPSM_ERR_CUDA;
-  CUtensorMap smap;
-  if (int r = make_stage_map(&smap, gram, F, Np, ld, gram_stride)) return r;
   int grid = (tasks + NG - 1) / NG;
   if (grid > num_sms()) grid = num_sms();
   if (const char* cap = getenv("KAPSM_GRID_CAP"))
     if (atoi(cap) > 0 && grid > atoi(cap)) grid = atoi(cap);
   kern<<<grid, Roles<NG>::WARPS * 32, smem, s>>>(
       gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, targets, F, K, Np, W,
-      (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status, dbg,
-      smap);
+      (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status, dbg);
   return status_from(cudaGetLastError());
 }
 
@@ -927,6 +867,10 @@ int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long 
                                   samples_stride, dim, targets, F, K, Np, W, eps, p, qtab,    \
                                   base0, theta0, coeff, first_step, theta, n_active, status, dbg, var)
   // the window dot covers the WM newest slots (static per unrolled step)
+#ifdef KAPSM_EXP_ONLY
+  if (W == 20) KAPSM_LT(20);
+  return KAPSM_ERR_UNSUPPORTED;
+#endif
   if (W <= 8) KAPSM_LT(8);
   if (W <= 16) KAPSM_LT(16);
   if (W <= 20) KAPSM_LT(20);
@@ -963,6 +907,9 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
     return launch_train_w<T, 1>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
                                 samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
                                 theta0, coeff, first_step, theta, n_active, status, dbg, var);
+#ifdef KAPSM_EXP_ONLY
+  return KAPSM_ERR_UNSUPPORTED;
+#endif
   if constexpr (sizeof(T) == 8) return KAPSM_ERR_UNSUPPORTED;
   else
     return launch_train_w<T, 4>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,

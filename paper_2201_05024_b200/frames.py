@@ -59,7 +59,9 @@ class FramePipeline:
         self.pilots = z(F, K, n_train, 2)
         self.tx = z(F, K, n_data, dt=torch.uint8)
         self.ld = _ld(self.Np)
-        self.gram = z(F, self.Np, self.ld)
+        # Gram workspace + the trainer's zero tail rows (kapsm_b200.h)
+        self._gram_buf = z(F * self.Np + 32, self.ld)
+        self.gram = self._gram_buf[: F * self.Np].view(F, self.Np, self.ld)
         self.coeff = z(F, K, self.Np)
         self.first_step = z(F, K, self.Np, dt=torch.int32)
         self.theta = z(F, K, 2 * M)
