@@ -298,3 +298,58 @@ KAPSM_DEV bool vote_all(bool p) {
   return r != 0;
 }
 }  // namespace kapsm
+
+namespace kapsm {
+// ---- thread-block clusters / distributed shared memory ----
+KAPSM_DEV unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same offset in CTA `rank` of this cluster
+KAPSM_DEV unsigned map_rank(unsigned local_addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+KAPSM_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// tagged stores through a shared::cluster address (local or a peer CTA)
+KAPSM_DEV void st_tag_cl(unsigned a, float v, int tag) {
+  unsigned long long w = ((unsigned long long)(unsigned)tag << 32) | __float_as_uint(v);
+  asm volatile("st.volatile.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(w) : "memory");
+}
+KAPSM_DEV void st_tag_cl(unsigned a, double v, int tag) {
+  asm volatile("st.volatile.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(a),
+               "l"(__double_as_longlong(v)), "l"((unsigned long long)(unsigned)tag)
+               : "memory");
+}
+KAPSM_DEV void st_cl_s32(unsigned a, int v) {
+  asm volatile("st.volatile.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+}  // namespace kapsm
+
+namespace kapsm {
+KAPSM_DEV void red_or_cl(unsigned a, int v) {
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+KAPSM_DEV int ld_cl_s32(unsigned a) {
+  int v;
+  asm volatile("ld.volatile.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+}  // namespace kapsm
+
+namespace kapsm {
+template <typename T> KAPSM_DEV void lds_quad(unsigned a, T (&v)[4]);
+template <> KAPSM_DEV void lds_quad<float>(unsigned a, float (&v)[4]) {
+  const float4 q = lds_f4(a);
+  v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+template <> KAPSM_DEV void lds_quad<double>(unsigned a, double (&v)[4]) {
+  const double2 p = lds_d2(a), q = lds_d2(a + 16);
+  v[0] = p.x; v[1] = p.y; v[2] = q.x; v[3] = q.y;
+}
+}  // namespace kapsm

@@ -54,12 +54,8 @@ constexpr int TC_BT = 4;                    // batch: takeover / entry / publica
 constexpr int TC_MAX_W = 24;                // lookahead D >= 4 with D + W <= 29
 constexpr int TC_PF = 2;                    // column prefetch distance (batches)
 constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2 > PF)
-constexpr int TC_TAIL_ROWS = 32;            // zero Gram rows required past the last frame
-constexpr int TC_SNAP = 8;                  // coefficient snapshots (ring of batches)
 constexpr int TC_INIT = 64;                 // init values (ring, pow2)
-constexpr int TC_Q = 64;                    // init part A covers i <= m - Q
-constexpr int TC_LAG = 3;                   // background: part A runs LAG tasks ahead of B
-constexpr int TC_ARING = 4;                 // part-A results in flight per warp (> LAG)
+constexpr int TC_Q = 61;                    // init: early part i <= m - Q, late part <= 32 elements
 constexpr int TC_MAX_NP = 3072;
 // slot reuse: the batch taken over after step n (samples n+D..n+D+3) reuses
 // the slots of samples that left the window by step n: D + 3 + W - 33 <= 0.
@@ -239,6 +235,50 @@ KAPSM_DEV double tagged_partial<double>(const double* row, const Tagged<double>:
   return s0 + s1;
 }
 
+// 16-byte vectors for the background row dots
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+KAPSM_DEV float4 ldg16(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+KAPSM_DEV double2 ldg16(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+template <typename T> KAPSM_DEV typename Vec16<T>::type lds16(unsigned a);
+template <> KAPSM_DEV float4 lds16<float>(unsigned a) { return lds_f4(a); }
+template <> KAPSM_DEV double2 lds16<double>(unsigned a) { return lds_d2(a); }
+KAPSM_DEV float dot16(const float4& c, const float4& r, float acc) {
+  return fmaf(c.w, r.w, fmaf(c.z, r.z, fmaf(c.y, r.y, fmaf(c.x, r.x, acc))));
+}
+KAPSM_DEV double dot16(const double2& c, const double2& r, double acc) {
+  return fma(c.y, r.y, fma(c.x, r.x, acc));
+}
+KAPSM_DEV float elem16(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+KAPSM_DEV double elem16(const double2& v, int e) { return e == 0 ? v.x : v.y; }
+
+// acc + sum_e c[i0+e] * r.e over EPV tagged coefficient slots at address a
+template <typename T>
+KAPSM_DEV T tagged_dot16(unsigned a, int i0, const typename Vec16<T>::type& r, T acc, bool& bad);
+template <>
+KAPSM_DEV float tagged_dot16<float>(unsigned a, int i0, const float4& r, float acc, bool& bad) {
+  uint4 p, q;
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(p.x), "=r"(p.y), "=r"(p.z), "=r"(p.w) : "r"(a) : "memory");
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a + 16) : "memory");
+  bad |= (int)p.y != i0 || (int)p.w != i0 + 1 || (int)q.y != i0 + 2 || (int)q.w != i0 + 3;
+  acc = fmaf(__uint_as_float(p.x), r.x, acc);
+  acc = fmaf(__uint_as_float(p.z), r.y, acc);
+  acc = fmaf(__uint_as_float(q.x), r.z, acc);
+  return fmaf(__uint_as_float(q.z), r.w, acc);
+}
+template <>
+KAPSM_DEV double tagged_dot16<double>(unsigned a, int i0, const double2& r, double acc, bool& bad) {
+  double v0, v1;
+  int t0, t1;
+  ld_tagged(a, v0, t0);
+  ld_tagged(a + 16, v1, t1);
+  bad |= t0 != i0 || t1 != i0 + 1;
+  return fma(v1, r.y, fma(v0, r.x, acc));
+}
+
 // Per-lane partial of sum_{i=0..last} c_i row[i] over plain arrays (the
 // caller has seen c_last published; earlier coefficients were stored first).
 KAPSM_DEV float plain_partial(const float* row, const float* cf, int last, int lane) {
@@ -282,36 +322,43 @@ KAPSM_DEV double slot_value<double>(const Tagged<double>::slot_t& w) {
   return __longlong_as_double((long long)w.v);
 }
 
-// Role layout of a CTA with NG groups.
-//   NG = 1 (latency): 7 warps; warp 3 (alone on sub-partition 3) is critical,
-//          warps 0,1,2,4,5,6 are background 0..5.
-//   NG = 4 (throughput): 16 warps; group g = w % 4, role w / 4 (3 = critical).
-template <int NG> struct Roles;
-template <> struct Roles<1> {
-  static constexpr int NB = 6, NBUF = 2, WARPS = 7;
+// Role layout.  CL = cluster size (CTAs per task group).
+//   NG = 1, CL = 2 (latency): a 2-CTA cluster per task.  CTA rank 0 runs only
+//          the critical warp (warp 7; the other warps wait for the
+//          epilogue), CTA rank 1 runs 8 background warps on another SM, so
+//          nothing competes with the critical warp for issue slots or the
+//          shared-memory pipe.  They exchange snapshots, final coefficients
+//          and init values through distributed shared memory.
+//   NG = 4, CL = 1 (throughput): group g = w % 4 on sub-partition g, role
+//          w / 4 (3 = critical).
+template <int NG, int CL> struct Roles;
+// Every role: NB = id of the critical role; NA A workers, NBH B helpers.
+// Every role: NB = id of the critical role, NA init workers (ids 0..NA-1).
+template <> struct Roles<1, 2> {
+  static constexpr int NB = 8, NA = 8, ACH = 12, WARPS = 8;   // ACH: row vectors per lane
   static KAPSM_DEV int group(int) { return 0; }
-  static KAPSM_DEV int role(int w) { return w == 3 ? NB : (w < 3 ? w : w - 1); }
+  // rank 0: warp 7 critical, warps 0..6 idle until the epilogue; rank 1: workers
+  static KAPSM_DEV int role(int w, unsigned rank) { return rank ? w : (w == 7 ? NB : -1); }
+  static KAPSM_DEV int a_index(int role) { return role; }
 };
-template <> struct Roles<4> {
-  static constexpr int NB = 3, NBUF = 1, WARPS = 16;
+template <> struct Roles<4, 1> {
+  static constexpr int NB = 3, NA = 3, ACH = 4, WARPS = 16;
   static KAPSM_DEV int group(int w) { return w & 3; }
-  static KAPSM_DEV int role(int w) { return w >> 2; }
+  static KAPSM_DEV int role(int w, unsigned) { return w >> 2; }   // 0..2 workers, 3 critical
+  static KAPSM_DEV int a_index(int role) { return role; }
 };
 
-template <typename T, int NG>
+template <typename T, int NG, int CL>
 struct GroupSmem {
   // byte offsets of one group's region in dynamic shared memory
-  size_t mbar, dv, snap, stage, initr, ctag, cfin, fsfin, bsm, qsm, apart, rows, ctl, total;
-  int npr;   // elements per Gram-row buffer
+  size_t dv, snap, stage, initr, ctag, cfin, fsfin, bsm, qsm, ctl, total;
   __host__ __device__ GroupSmem(int W, int Np) {
     using Slot = typename Tagged<T>::slot_t;
-    constexpr int NB = Roles<NG>::NB, NBUF = Roles<NG>::NBUF;
+    constexpr int NB = Roles<NG, CL>::NB;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 15) & ~size_t(15); return r; };
-    npr = (Np + 8 + 7) & ~7;
-    mbar = take(NB * NBUF * sizeof(unsigned long long));
     dv = take(2 * TC_S * sizeof(T));
-    snap = take((size_t)TC_SNAP * TC_S * sizeof(Slot));
+    snap = take((size_t)2 * TC_S * sizeof(T));   // slot coefficients after a block's 1st step
     stage = take((size_t)TC_SRING * TC_BT * TC_S * sizeof(T));
     initr = take((size_t)TC_INIT * sizeof(Slot));
     ctag = take((size_t)(Np + TC_S) * sizeof(Slot));
@@ -319,8 +366,6 @@ struct GroupSmem {
     fsfin = take((size_t)(Np + TC_S) * sizeof(int));
     bsm = take((size_t)(Np + 2 * TC_S) * sizeof(T));
     qsm = take(2 * (size_t)(W + 1) * sizeof(T));
-    apart = take((size_t)NB * TC_ARING * sizeof(T));
-    rows = take((size_t)NB * NBUF * npr * sizeof(T));
     ctl = take(16 * sizeof(int));
     total = (o + 127) & ~size_t(127);
   }
@@ -344,8 +389,8 @@ __device__ __noinline__ void init_spin(unsigned a, bool isent, int me, int Np, T
   }
 }
 
-template <typename T, int NG, int WM, bool DBG>
-__global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
+template <typename T, int NG, int CL, int WM, bool DBG>
+__global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
     apsm_train_kernel(const T* __restrict__ gram, long long ld, long long gram_stride,
                       const T* __restrict__ rx, long long rx_stride,
                       const T* __restrict__ samples, long long samples_stride, int dim,
@@ -356,34 +401,50 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
                       int* __restrict__ nact_out, int* __restrict__ status_out,
                       long long* __restrict__ dbg) {
   using Slot = typename Tagged<T>::slot_t;
-  using R = Roles<NG>;
-  constexpr int NB = R::NB, NBUF = R::NBUF;
+  using R = Roles<NG, CL>;
+  constexpr int NB = R::NB, ACH = sizeof(T) == 8 ? R::ACH / 2 : R::ACH;
   constexpr int D = lookahead(WM);            // takeover lookahead (steps)
   constexpr int FEAT = KAPSM_FEAT;            // experiments only: parts compiled out
   constexpr int FIRST = D;                    // first sample whose init needs coefficients
   constexpr unsigned TS = sizeof(T), SS = sizeof(Slot);
   extern __shared__ __align__(128) unsigned char smem[];
-  const GroupSmem<T, NG> L(W, Np);
+  const GroupSmem<T, NG, CL> L(W, Np);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rank = CL > 1 ? cluster_rank() : 0u;
   const int grp = R::group(warp);
-  const int role = R::role(warp);              // 0..NB-1: background, NB: critical
-  const int gt = role * 32 + lane;             // thread index inside the group
-  constexpr int GT = (NB + 1) * 32;
+  const int role = R::role(warp, rank);        // 0..NB-1: background, NB: critical, -1: idle
+  // threads sharing this group's shared-memory region (per-task init, epilogue)
+  const int gt = NG == 1 ? (int)threadIdx.x : role * 32 + lane;
+  constexpr int GT = NG == 1 ? R::WARPS * 32 : (NB + 1) * 32;
   unsigned char* gs = smem + (size_t)grp * L.total;
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(gs + L.mbar);
-  Slot* snap = reinterpret_cast<Slot*>(gs + L.snap);     // [SNAP][S] tagged c snapshots
+  // shared::cluster bases of this group's region in the critical CTA and in
+  // the background CTA (the same CTA unless CL = 2)
+  const unsigned lbase = smem_u32(gs);
+  const unsigned cw_base = CL > 1 ? map_rank(lbase, 0) : lbase;
+  const unsigned bg_base = CL > 1 ? map_rank(lbase, CL - 1) : lbase;
   Slot* initr = reinterpret_cast<Slot*>(gs + L.initr);   // [INIT] tagged init_m
   Slot* ctag = reinterpret_cast<Slot*>(gs + L.ctag);     // [Np+S] tagged final c_m
   T* cfin = reinterpret_cast<T*>(gs + L.cfin);           // [Np+S] final c_m (stored before ctag)
   int* fsfin = reinterpret_cast<int*>(gs + L.fsfin);     // [Np+S] first-activation step
   T* bsm = reinterpret_cast<T*>(gs + L.bsm);             // [Np+2S] targets (zero padded)
   T* qsm = reinterpret_cast<T*>(gs + L.qsm);             // [W+1][2] (q_mid, q_last), row W = 0
-  T* rows = reinterpret_cast<T*>(gs + L.rows);           // [NB][NBUF][npr] Gram rows (TMA)
   int* ctl = reinterpret_cast<int*>(gs + L.ctl);         // [1]=abort [2]=status [3]=nact
   const int group_bar = 1 + grp;
   const int dbgvar = DBG ? (int)dbg[5 * Np] : 0;
+  auto group_sync = [&] {
+    if constexpr (CL > 1) cluster_sync();
+    else named_bar(group_bar, GT);
+  };
+  // abort: raise the flag in both CTAs
+  auto raise_abort = [&](int code) {
+    red_or_cl(cw_base + (unsigned)L.ctl + 8u, code);
+    st_cl_s32(cw_base + (unsigned)L.ctl + 4u, 1);
+    if (CL > 1) st_cl_s32(bg_base + (unsigned)L.ctl + 4u, 1);
+  };
+  const int ncl = CL > 1 ? (int)gridDim.x / CL : (int)gridDim.x;
+  const int cid = CL > 1 ? (int)blockIdx.x / CL : (int)blockIdx.x;
 
-  for (int task = blockIdx.x * NG + grp; task < F * K; task += gridDim.x * NG) {
+  for (int task = cid * NG + grp; task < F * K; task += ncl * NG) {
     const int fu = task;                        // frame * K + user
     const int f = fu / K;
     const T* G = gram + (long long)f * gram_stride;
@@ -391,7 +452,6 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     const T* P0 = base0 ? base0 + (long long)fu * Np : nullptr;
 
     // ---------------- per-task group state ----------------
-    for (int i = gt; i < TC_SNAP * TC_S; i += GT) Tagged<T>::store(&snap[i], T(0), -1);
     for (int i = gt; i < TC_INIT; i += GT) Tagged<T>::store(&initr[i], T(0), -1);
     for (int i = gt; i < Np + TC_S; i += GT) { Tagged<T>::store(&ctag[i], T(0), -1); fsfin[i] = -1; }
     for (int i = gt; i < Np + 2 * TC_S; i += GT) bsm[i] = i < Np ? B[i] : T(0);
@@ -403,11 +463,7 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       qsm[2 * i + 1] = ql;
     }
     if (gt < 16) ctl[gt] = 0;
-    if (gt == 0) {
-      for (int r = 0; r < NB * NBUF; ++r) mbar_init(&mbar[r], 1);
-      mbar_fence_init();
-    }
-    named_bar(group_bar, GT);
+    group_sync();
 
     if (role == NB) {
       // =========================== CRITICAL WARP ===========================
@@ -420,10 +476,13 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       const int x = lane;
       const unsigned gbase = opaque_u32(smem_u32(gs));
       const unsigned dv_s = gbase + (unsigned)L.dv, stage_s = gbase + (unsigned)L.stage;
-      const unsigned snap_s = gbase + (unsigned)L.snap + x * SS;
+      const unsigned snap_s = gbase + (unsigned)L.snap;
       const unsigned initr_s = gbase + (unsigned)L.initr, ctag_s = gbase + (unsigned)L.ctag;
       const unsigned fsfin_s = gbase + (unsigned)L.fsfin, bsm_s = gbase + (unsigned)L.bsm;
       const unsigned qsm_s = gbase + (unsigned)L.qsm, cfin_s = gbase + (unsigned)L.cfin;
+      // the background CTA's copies (shared::cluster addresses)
+      // the A workers' copy of the final coefficients (shared::cluster address)
+      const unsigned bctag_s = opaque_u32(bg_base + (unsigned)L.ctag);
       const int Wm1 = W - 1;
       constexpr int NOWN = D;                   // samples owned from the start
 
@@ -540,7 +599,7 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         if (n >= nend) return false;
         const int jb = n >> 2;
         auto mark = [&](int idx) {
-          if (DBG && (dbgvar & 4) && lane == 0 && fu == 0) dbg[6 * Np + jb * 8 + idx] = clock64();
+          if (DBG && (dbgvar & 4) && lane == 0 && fu == 0) dbg[7 * Np + jb * 8 + idx] = clock64();
         };
         const int rel = (x - (k0 + D)) & (TC_S - 1);
         const bool isnew = rel < TC_BT;                       // slot taken over in this block
@@ -559,10 +618,12 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
           if ((unsigned)(n - mleave) < (unsigned)TC_BT && m >= 0) {
             sts(cfa, c);
             st_tag(cta, c, m);
+            if (CL > 1) st_tag_cl(bctag_s + (cta - ctag_s), c, m);
             sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
           }
-          // ---- snapshot c^(n+1) for the init of the batch taken over now ----
-          st_tag(snap_s + (jb & (TC_SNAP - 1)) * TC_S * SS, c, n + 1);
+          // ---- c^(n+1) of the slots that stay (the batch's slots give 0):
+          //      the new samples' responses to them are formed in this warp ----
+          sts(snap_s + ((jb & 1) * TC_S + x) * TS, isnew ? T(0) : c);
         }
         warp_sync_full();                                     // staged batch visible to all
         mark(1);
@@ -604,10 +665,29 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         mark(3);
         // ---- step n+2: entry check of the next block's samples, staging of a
         //      later batch ----
+        // ---- step n+2: entry check of the next block's samples; the new
+        //      slots' response to the coefficients that stay in the slots
+        //      (sum_l c_l^(n+1) K[sample(l)][mt], the in-slot part of init_mt) ----
+        T yinit = T(0);
         step(n + 2, ic<(k0 + 2) & 31>{}, false, [&] {
           if (!(FEAT & 32)) weights(n + 3, qcm[2], qcl[2]);
           if (!(FEAT & 16)) init_check(n + TC_BT);
+          if (!(FEAT & 2)) {
+            const unsigned cs = snap_s + (jb & 1) * TC_S * TS;
+            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              T c4[4];
+              lds_quad<T>(cs + 4 * q * TS, c4);
+              a0 = fma(c4[0], row[4 * q], a0);
+              a1 = fma(c4[1], row[4 * q + 1], a1);
+              a2 = fma(c4[2], row[4 * q + 2], a2);
+              a3 = fma(c4[3], row[4 * q + 3], a3);
+            }
+            yinit = (a0 + a1) + (a2 + a3);
+          }
         });
+        if (isnew) { bme -= yinit; bpe -= yinit; bm -= yinit; bp -= yinit; }
         if (!(FEAT & 8)) stage_issue(jb + TC_PF);
         mark(4);
         step(n + 3, ic<(k0 + 3) & 31>{}, false, [&] {
@@ -633,132 +713,135 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
       // samples still in the window after the last step: coefficients final now
       if (!aborted && nlast >= 0 && m >= 0 && m < Np && mleave > nlast) {
         sts(cfa, c);
-        st_tag(cta, c, m);
         sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
       }
       const bool any_degen = __any_sync(0xffffffffu, degen != 0);
       __syncwarp();
       if (lane == 0) {
         if (any_degen) atomicOr(&ctl[2], KAPSM_TRAIN_DEGENERATE);
-        if (aborted) { atomicOr(&ctl[2], KAPSM_TRAIN_STALLED); st_volatile(&ctl[1], 1); }
+        if (aborted) raise_abort(KAPSM_TRAIN_STALLED);
       }
-    } else if (!(DBG && (dbgvar & 2)) && !(FEAT & 128)) {
-      // ========================== BACKGROUND WARPS =========================
-      // Warp j computes init_m for the samples m_t = FIRST + j + t*NB, with
-      // n_m = (m-D) & ~3 the step from which m's slot accumulates:
-      //   init_m = f0(r_m) + sum_{i <= m-Q} cfinal_i K[m][i]                  (A)
-      //          + sum_{m-Q < i < n_m} c_i^(n_m) K[m][i]                       (B)
-      // A only needs coefficients that are final long before m is taken over,
-      // so each warp runs A TC_LAG tasks ahead of B (software pipeline); B
-      // reads final coefficients (i <= n_m - W) or the snapshot taken at the
-      // start of step n_m.  A's Gram row prefix arrives by TMA bulk copy, B's
-      // 64 entries by plain loads issued one A-task ahead.
-      const int j = role;
+    } else if (role >= 0 && !(DBG && (dbgvar & 2)) && !(FEAT & 128)) {
+      // ============================ INIT WORKERS ============================
+      // The batch of sample m is taken over after step n_m = (m-D) & ~3; the
+      // critical warp itself forms the new slot's response to the coefficients
+      // that stay in the slots (samples n_m+D-28 .. n_m).  Everything older is
+      // final by then, and the init workers (the other CTA of the cluster when
+      // CL = 2) supply
+      //   init_m = f0(r_m) + sum_{i <= lastF} cfinal_i K[m][i],  lastF = n_m + D - 29,
+      // as an early part over i <= m - Q (final ~Q-W steps before m is taken
+      // over: its Gram row is streamed from L2 into registers, double
+      // buffered) plus a late part over (m - Q, lastF] (one element per lane)
+      // once c_lastF is published, and push it into the critical CTA's ring.
+      const int j = R::a_index(role);
+      constexpr int nw = R::NA;
       const unsigned gbase = smem_u32(gs);
-      const unsigned snap_s = gbase + (unsigned)L.snap, ctag_s = gbase + (unsigned)L.ctag;
-      const unsigned initr_s = gbase + (unsigned)L.initr;
-      T* apart = reinterpret_cast<T*>(gs + L.apart) + j * TC_ARING;
-      if (j == 0)
-        for (int i = lane; i < FIRST && i < Np; i += 32)
-          st_tag(initr_s + (i & (TC_INIT - 1)) * SS, P0 ? P0[i] : T(0), i);
-      T* bufs = rows + (size_t)j * NBUF * L.npr;
-      unsigned long long* bars = mbar + j * NBUF;
-      auto mtask = [&](int t) { return FIRST + j + t * NB; };
-      // TMA of row m's prefix [0, m-Q] (A's operand)
-      auto issue_row = [&](int t) {
-        const int mt = mtask(t);
-        if (mt >= Np || mt - TC_Q < 0) return;
-        const int slot = t % NBUF;
-        const unsigned bytes = (unsigned)(((mt - TC_Q + 1) * (int)sizeof(T) + 15) & ~15);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[slot], bytes);
-        tma_bulk_g2s(bufs + (size_t)slot * L.npr, G + (long long)mt * ld, bytes, &bars[slot]);
-      };
-      if (lane == 0)
-        for (int t = 0; t < NBUF; ++t) issue_row(t);
-      unsigned phases = 0;
+      const unsigned ctag_s = gbase + (unsigned)L.ctag;
+      const unsigned cinitr_s = cw_base + (unsigned)L.initr;   // the critical CTA's ring
+      auto mtask = [&](int t) { return FIRST + j + t * nw; };
       bool stop = false;
-      // (A) of task t: partial dot -> apart[t % ARING] (lane 0)
-      auto part_a = [&](int t) {
+      if (j == 0)                                          // f0 only before any update
+        for (int i = lane; i < FIRST && i < Np; i += 32)
+          st_tag_cl(cinitr_s + (i & (TC_INIT - 1)) * SS, P0 ? P0[i] : T(0), i);
+      using V16 = typename Vec16<T>::type;                 // 16-byte vector of T
+      constexpr int EPV = 16 / sizeof(T);
+      constexpr int CH = 32 * EPV * ACH;                   // row elements per register chunk
+      V16 ra0[ACH], ra1[ACH];
+      T kl0 = T(0), kl1 = T(0);                            // late-part Gram entry per lane
+      auto a_issue = [&](V16 (&ra)[ACH], int mt, int lastA, int c0) {
+        const T* rowp = G + (long long)mt * ld;
+#pragma unroll
+        for (int u = 0; u < ACH; ++u) {
+          const int i = c0 + (u * 32 + lane) * EPV;
+          if (i <= lastA) ra[u] = ldg16(rowp + i);
+        }
+      };
+      // chunk c0 against the published final coefficients (tagged; a tag not
+      // yet visible makes the chunk redo)
+      auto a_dot = [&](const V16 (&ra)[ACH], int lastA, int c0) -> T {
+        for (;;) {
+          T acc0 = T(0), acc1 = T(0);
+          bool bad = false;
+#pragma unroll
+          for (int u = 0; u < ACH; ++u) {
+            const int i = c0 + (u * 32 + lane) * EPV;
+            if (i + EPV - 1 <= lastA) {
+              acc0 = tagged_dot16<T>(ctag_s + i * SS, i, ra[u], acc0, bad);
+            } else if (i <= lastA) {
+              for (int e = 0; e < EPV && i + e <= lastA; ++e) {
+                T cv;
+                bad |= !ld_tag(ctag_s + (i + e) * SS, i + e, cv);
+                acc1 = fma(cv, elem16(ra[u], e), acc1);
+              }
+            }
+          }
+          if (!__any_sync(0xffffffffu, bad)) return acc0 + acc1;
+        }
+      };
+      auto wait_final = [&](int i) {                      // c_i published?
+        T cl;
+        long long spins = 0;
+        while (!stop && !ld_tag(ctag_s + i * SS, i, cl))
+          if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1])))
+          { stop = true; red_or_cl(cw_base + (unsigned)L.ctl + 8u, 32); }
+        if (__any_sync(0xffffffffu, stop)) stop = true;
+      };
+      // the critical warp covers the slots that stay through the takeover:
+      // samples n_m+D-28 .. n_m; the taken-over slots' old samples and all
+      // older ones are final by then
+      auto lastf = [&](int mt) { return ((mt - D) & ~(TC_BT - 1)) + D - TC_S + TC_BT - 1; };
+      auto a_start = [&](V16 (&ra)[ACH], T& kl, int t) {
         const int mt = mtask(t);
         if (mt >= Np) return;
-        T a = T(0);
-        const int lastA = mt - TC_Q;
-        if (lastA >= 0) {
-          const int slot = t % NBUF;
-          {
-            long long spins = 0;
-            while (!mbar_try_wait(&bars[slot], (phases >> slot) & 1u))
-              if (++spins > TC_SPIN_LIMIT) { stop = true; atomicOr(&ctl[2], 16); break; }
-            phases ^= 1u << slot;
-          }
-          {
-            T cl;
-            long long spins = 0;
-            while (!stop && !ld_tag(ctag_s + lastA * SS, lastA, cl))
-              if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1])))
-              { stop = true; atomicOr(&ctl[2], 32); }
-          }
-          if (__any_sync(0xffffffffu, stop)) { stop = true; return; }
-          const T* buf = bufs + (size_t)slot * L.npr;
-          a = warp_sum(plain_partial(buf, cfin, lastA, lane));
-        }
-        __syncwarp();                                    // every lane is done with buf
-        if (lane == 0) {
-          issue_row(t + NBUF);                           // refill this task's buffer slot
-          apart[t % TC_ARING] = a;
-        }
+        if (mt - TC_Q >= 0) a_issue(ra, mt, mt - TC_Q, 0);
+        const int i = mt - TC_Q + 1 + lane;                // late part: one element per lane
+        kl = (i >= 0 && i <= lastf(mt)) ? G[(long long)mt * ld + i] : T(0);
       };
-      for (int t = 0; t < TC_LAG; ++t) part_a(t);
-      for (int t = 0; !stop; ++t) {
+      auto a_finish = [&](V16 (&ra)[ACH], T kl, int t) -> bool {
         const int mt = mtask(t);
-        if (mt >= Np) break;
-        const int nm = (mt - D) & ~(TC_BT - 1);    // its batch is taken over after step nm
-        // B's Gram entries (2 per lane), loaded ahead of the A task below
-        T kb[2];
-        int ib[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          ib[h] = mt - TC_Q + 1 + lane + 32 * h;
-          kb[h] = (ib[h] >= 0 && ib[h] <= nm) ? G[(long long)mt * ld + ib[h]] : T(0);
-        }
-        const T f0m = P0 ? P0[mt] : T(0);
-        if (DBG && lane == 0 && fu == 0) dbg[3 * Np + mt] = clock64();
-        part_a(t + TC_LAG);
-        if (stop) break;
-        if (DBG && lane == 0 && fu == 0) dbg[4 * Np + mt] = clock64();
+        if (mt >= Np) return false;
+        const int lastA = mt - TC_Q, lastF = lastf(mt);
         T part = T(0);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {                      // (B)
-          const int i = ib[h];
-          if (i >= 0 && i <= nm) {
-            const bool fin = i <= nm - W + 1;            // published before the snapshot
-            const unsigned a = fin ? ctag_s + i * SS
-                                   : snap_s + (((nm >> 2) & (TC_SNAP - 1)) * TC_S + (i & (TC_S - 1))) * SS;
-            const int tag = fin ? i : nm + 1;
-            T cv;
-            long long spins = 0;
-            while (!ld_tag(a, tag, cv))
-              if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1]))) {
-                stop = true; atomicOr(&ctl[2], 64);
-                break;
-              }
-            part = fma(cv, kb[h], part);
+        if (lastA >= 0) {                                  // early part
+          wait_final(lastA);
+          if (stop) return false;
+          part = a_dot(ra, lastA, 0);
+          for (int c0 = CH; c0 <= lastA; c0 += CH) {        // rows longer than one chunk
+            a_issue(ra, mt, lastA, c0);                     // (the consumed buffer is reused)
+            part += a_dot(ra, lastA, c0);
           }
         }
-        if (__any_sync(0xffffffffu, stop)) { stop = true; break; }
-        const T tot = warp_sum(part) + f0m;
-        if (lane == 0) st_tag(initr_s + (mt & (TC_INIT - 1)) * SS, tot + apart[t % TC_ARING], mt);
-        if (DBG && lane == 0 && fu == 0) dbg[2 * Np + mt] = clock64();
+        if (lastF >= 0) {                                  // late part
+          wait_final(lastF);
+          if (stop) return false;
+          const int i = mt - TC_Q + 1 + lane;
+          for (;;) {
+            T cv = T(0);
+            bool bad = false;
+            if (i >= 0 && i <= lastF) bad = !ld_tag(ctag_s + i * SS, i, cv);
+            if (!__any_sync(0xffffffffu, bad)) { part = fma(cv, kl, part); break; }
+          }
+        }
+        const T tot = warp_sum(part) + (P0 ? P0[mt] : T(0));
+        if (lane == 0) st_tag_cl(cinitr_s + (mt & (TC_INIT - 1)) * SS, tot, mt);
+        return true;
+      };
+      a_start(ra0, kl0, 0);
+      for (int t = 0; !stop; t += 2) {                      // unrolled by 2: buffers swap
+        a_start(ra1, kl1, t + 1);
+        if (!a_finish(ra0, kl0, t)) break;
+        a_start(ra0, kl0, t + 2);
+        if (!a_finish(ra1, kl1, t + 1)) break;
       }
-      if (stop && lane == 0) { atomicOr(&ctl[2], KAPSM_TRAIN_STALLED); st_volatile(&ctl[1], 1); }
+      if (stop && lane == 0) raise_abort(KAPSM_TRAIN_STALLED);
     }
-    named_bar(group_bar, GT);
+    group_sync();
+    if (CL > 1 && rank != 0) continue;          // the epilogue runs in the critical CTA
     // ---- outputs: coefficients, first steps (coalesced), activation count ----
     {
       int na = 0;
       for (int i = gt; i < Np; i += GT) {
-        coeff_out[(long long)fu * Np + i] = slot_value<T>(ctag[i]);
+        coeff_out[(long long)fu * Np + i] = cfin[i];
         const int v = fsfin[i];
         fs_out[(long long)fu * Np + i] = v;
         na += (v >= 0);
@@ -770,15 +853,16 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     {
       T* th = theta_out + (long long)fu * dim;
       const T* t0 = theta0 ? theta0 + (long long)fu * dim : nullptr;
-      constexpr int nw = NB + 1;
+      constexpr int nw = NG == 1 ? R::WARPS : NB + 1;
+      const int ew = NG == 1 ? warp : role;
       if (rx) {
         // complex pilots: Theta = theta[:M] + i theta[M:] = w_l sum_p (c_2p - i c_2p+1) x_p
         const int M = dim / 2, n_train = Np / 2;
         const T* X = rx + (long long)f * rx_stride;
-        for (int kk = role; kk < M; kk += nw) {
+        for (int kk = ew; kk < M; kk += nw) {
           T tr = T(0), ti = T(0);
           for (int p = lane; p < n_train; p += 32) {
-            const T c1 = slot_value<T>(ctag[2 * p]), c2 = slot_value<T>(ctag[2 * p + 1]);
+            const T c1 = cfin[2 * p], c2 = cfin[2 * p + 1];
             const T xr = X[(long long)p * 2 * M + 2 * kk], xi = X[(long long)p * 2 * M + 2 * kk + 1];
             tr = fma(c1, xr, fma(c2, xi, tr));
             ti = fma(c1, xi, fma(-c2, xr, ti));
@@ -792,9 +876,9 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
         }
       } else {
         const T* S = samples + (long long)f * samples_stride;
-        for (int kk = role; kk < dim; kk += nw) {
+        for (int kk = ew; kk < dim; kk += nw) {
           T acc = T(0);
-          for (int i = lane; i < Np; i += 32) acc = fma(slot_value<T>(ctag[i]), S[(long long)i * dim + kk], acc);
+          for (int i = lane; i < Np; i += 32) acc = fma(cfin[i], S[(long long)i * dim + kk], acc);
           acc = warp_sum(acc);
           if (lane == 0) th[kk] = w_l * acc + (t0 ? t0[kk] : T(0));
         }
@@ -804,10 +888,6 @@ __global__ void __launch_bounds__(Roles<NG>::WARPS * 32, 1)
     if (gt == 0) {
       status_out[fu] = ctl[2];
       nact_out[fu] = ctl[3];
-    }
-    if (gt == 0) {                                 // barriers are re-initialised per task
-      for (int r = 0; r < NB * NBUF; ++r)
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mbar[r])) : "memory");
     }
     named_bar(group_bar, GT);                      // state reused by the next task
   }
@@ -824,48 +904,63 @@ static int num_sms() {
   return n;
 }
 
-template <typename T, int NG, int WM>
+template <typename T, int NG, int CL, int WM>
 int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long long gram_stride,
                  const T* rx, long long rx_stride, const T* samples, long long samples_stride,
                  int dim, const T* targets, int F, int K, int Np, int W, double eps,
                  kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
-                 int* first_step, T* theta, int* n_active, int* status, long long* dbg,
-                 int var) {
-  auto kern = apsm_train_kernel<T, NG, WM, false>;
+                 int* first_step, T* theta, int* n_active, int* status, long long* dbg) {
+  auto kern = apsm_train_kernel<T, NG, CL, WM, false>;
   if constexpr (sizeof(T) == 4 && NG == 1 && WM == 20) {   // clock instrumentation build
-    if (dbg) kern = apsm_train_kernel<T, NG, WM, true>;
+    if (dbg) kern = apsm_train_kernel<T, NG, CL, WM, true>;
   } else if (dbg) {
     return KAPSM_ERR_UNSUPPORTED;
   }
-  const GroupSmem<T, NG> L(W, Np);
+  const GroupSmem<T, NG, CL> L(W, Np);
   size_t smem = L.total * NG;
-  // NG = 1: pad shared memory so that only one CTA fits per SM
+  // NG = 1: pad shared memory so that only one CTA fits per SM (the two CTAs
+  // of a cluster land on different SMs)
   if (NG == 1 && smem < 120 * 1024) smem = 120 * 1024;
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return KAPSM_ERR_CUDA;
-  int grid = (tasks + NG - 1) / NG;
-  if (grid > num_sms()) grid = num_sms();
+  int groups = (tasks + NG - 1) / NG;                 // CTAs (CL = 1) or clusters (CL = 2)
+  const int max_groups = num_sms() / CL;
+  if (groups > max_groups) groups = max_groups;
   if (const char* cap = getenv("KAPSM_GRID_CAP"))
-    if (atoi(cap) > 0 && grid > atoi(cap)) grid = atoi(cap);
-  kern<<<grid, Roles<NG>::WARPS * 32, smem, s>>>(
-      gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, targets, F, K, Np, W,
-      (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status, dbg);
+    if (atoi(cap) > 0 && groups > atoi(cap)) groups = atoi(cap);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * CL);
+  cfg.blockDim = dim3(Roles<NG, CL>::WARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(
+      &cfg, kern, gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, targets, F,
+      K, Np, W, (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status,
+      dbg);
+  if (e != cudaSuccess) return KAPSM_ERR_CUDA;
   return status_from(cudaGetLastError());
 }
 
-template <typename T, int NG>
+template <typename T, int NG, int CL>
 int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long long gram_stride,
                    const T* rx, long long rx_stride, const T* samples, long long samples_stride,
                    int dim, const T* targets, int F, int K, int Np, int W, double eps,
                    kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
-                   int* first_step, T* theta, int* n_active, int* status, long long* dbg,
-                   int var) {
-#define KAPSM_LT(WMV)                                                                         \
-  return launch_train<T, NG, WMV>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,    \
-                                  samples_stride, dim, targets, F, K, Np, W, eps, p, qtab,    \
-                                  base0, theta0, coeff, first_step, theta, n_active, status, dbg, var)
+                   int* first_step, T* theta, int* n_active, int* status, long long* dbg) {
+#define KAPSM_LT(WMV)                                                                          \
+  return launch_train<T, NG, CL, WMV>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples, \
+                                      samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, \
+                                      base0, theta0, coeff, first_step, theta, n_active, status, \
+                                      dbg)
   // the window dot covers the WM newest slots (static per unrolled step)
 #ifdef KAPSM_EXP_ONLY
   if (W == 20) KAPSM_LT(20);
@@ -883,7 +978,7 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
           const T* samples, long long samples_stride, int dim, const T* targets, int F, int K,
           int Np, int W, double eps, kapsm_kernel_params p, const T* qtab, const T* base0,
           const T* theta0, T* coeff, int* first_step, T* theta, int* n_active, int* status,
-          cudaStream_t s, long long* dbg = nullptr, int var = 0) {
+          cudaStream_t s, long long* dbg = nullptr) {
   if (F < 0 || K < 1 || Np < 1 || dim < 1 || W < 1 || !(eps > 0)) return KAPSM_ERR_INVALID;
   if (F == 0) return KAPSM_OK;
   if (!gram || !targets || !coeff || !first_step || !theta || !n_active || !status)
@@ -891,30 +986,30 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
   if ((rx == nullptr) == (samples == nullptr)) return KAPSM_ERR_INVALID;  // exactly one source
   if (rx && ((Np & 1) || (dim & 1))) return KAPSM_ERR_INVALID;
   if (W > TC_MAX_W || Np > TC_MAX_NP) return KAPSM_ERR_UNSUPPORTED;
-  // TMA copies read whole 16-byte granules and the staged column segments run
-  // up to 11 columns past Np: rows need >= 16 (finite, zero) padding columns
+  // rows: 16-byte aligned with >= 16 padding columns (kapsm_b200.h)
   if (ld < Np + 16 || (ld * (long long)sizeof(T)) % 16 ||
       (gram_stride * (long long)sizeof(T)) % 16 || ((size_t)gram & 15))
     return KAPSM_ERR_INVALID;
   const int tasks = F * K;
-  // latency mode (one chain per SM) when the tasks fit on the SMs or 4 groups do not fit
-  // (FP64 is the parity/test precision: latency mode only)
+  // latency mode (a 2-CTA cluster per chain) while the chains fit twice on the
+  // SMs; throughput mode (4 chains per SM) beyond.  FP64 (the parity/test
+  // precision) always runs in latency mode.
   static const bool force_lat = getenv("KAPSM_FORCE_LATENCY_MODE") != nullptr;
   const bool lat = force_lat || sizeof(T) == 8 || tasks <= num_sms() ||
-                   GroupSmem<T, 4>(W, Np).total * 4 > 227 * 1024;
-  if (GroupSmem<T, 1>(W, Np).total > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
+                   GroupSmem<T, 4, 1>(W, Np).total * 4 > 227 * 1024;
+  if (GroupSmem<T, 1, 2>(W, Np).total > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (lat)
-    return launch_train_w<T, 1>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
-                                samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
-                                theta0, coeff, first_step, theta, n_active, status, dbg, var);
+    return launch_train_w<T, 1, 2>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
+                                   samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
+                                   theta0, coeff, first_step, theta, n_active, status, dbg);
 #ifdef KAPSM_EXP_ONLY
   return KAPSM_ERR_UNSUPPORTED;
 #endif
   if constexpr (sizeof(T) == 8) return KAPSM_ERR_UNSUPPORTED;
   else
-    return launch_train_w<T, 4>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
-                              samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
-                              theta0, coeff, first_step, theta, n_active, status, dbg, var);
+    return launch_train_w<T, 4, 1>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
+                                   samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
+                                   theta0, coeff, first_step, theta, n_active, status, dbg);
 }
 
 }  // namespace kapsm
@@ -947,8 +1042,8 @@ extern "C" int kapsm_internal_train_clock_f32(const float* gram, long long ld,
                                               const float* qtab, float* coeff, int* first_step,
                                               float* theta, int* n_active, int* status,
                                               long long* clocks, int variant, void* stream) {
+  (void)variant;
   return kapsm::train<float>(gram, ld, gram_stride, rx, rx_stride, nullptr, 0, dim, targets, F, K,
                              n_samples, window, epsilon, p, qtab, nullptr, nullptr, coeff,
-                             first_step, theta, n_active, status, (cudaStream_t)stream, clocks,
-                             variant);
+                             first_step, theta, n_active, status, (cudaStream_t)stream, clocks);
 }

@@ -14,7 +14,7 @@ fn.argtypes = [P, L, L, P, L, P, I, I, I, I, I, D, _lib.KernelParamsC, P, P, P, 
 rx, pil, tx, _ = K.host_frames([0], 6, 16, 685, 3840, "QPSK")
 pipe = K.FramePipeline(1, 6, 16, 685, 3840, "QPSK", precision="f32")
 pipe.load(rx, pil, tx); pipe.launch(); torch.cuda.synchronize()
-clk = torch.zeros(6 * pipe.Np + 8 * (pipe.Np // 4 + 2), dtype=torch.int64, device="cuda")
+clk = torch.zeros(7 * pipe.Np + 8 * (pipe.Np // 4 + 2), dtype=torch.int64, device="cuda")
 c = pipe.cfg
 variants = [int(v) for v in sys.argv[1:]] or [0]
 for var in variants:
@@ -33,16 +33,18 @@ for var in variants:
         print("  cycles/step: mean %.0f median %.0f p90 %.0f max %.0f | warm-up %.0f | steady %.0f | init spins %d" % (
             dt.mean(), np.median(dt), np.percentile(dt, 90), dt.max(), dt[:19].mean(), dt[64:].mean(), (sp > 0).sum()))
         print("  steps 64..96:", dt[64:96].tolist())
-        mk = allc[6*Np:6*Np + 8*(Np//4)].reshape(-1, 8)
+        mk = allc[7*Np:7*Np + 8*(Np//4)].reshape(-1, 8)
         print("  block marks (rel. to step n clock): [after step n, after publish/snap/wait, after step n+1, after takeover state+stage, after step n+2, after step n+3]")
         for jb in range(20, 26):
             print("   ", jb, (mk[jb, :6] - t[4*jb]).tolist(), "next block start", int(t[4*jb+4] - t[4*jb]))
         pub = allc[2*Np:3*Np]; bst = allc[3*Np:4*Np]; aend = allc[4*Np:5*Np]
         rows = []
-        for m in range(64, 200):
+        for m in range(400, 560):
             nm = (m - D) & ~3
-            snapt = t[nm] if nm < Np else 0
-            dead = t[(m & ~3) - 1] if (m & ~3) - 1 < Np else 0
-            rows.append((m, int(bst[m]-snapt), int(aend[m]-snapt), int(pub[m]-snapt), int(dead-snapt)))
-        print("  m, iterstart-snap, Aend-snap, publish-snap, deadline-snap")
-        for r in rows[:16]: print("   ", r)
+            snapt = t[nm + 1] if nm + 1 < Np else 0
+            dead = t[(m & ~3) - 2] if (m & ~3) - 2 < Np else 0
+            bdone = allc[5*Np+1+m]
+            rows.append((m, int(bst[m]-snapt), int(bdone-snapt), int(aend[m]-snapt), int(pub[m]-snapt), int(dead-snapt)))
+        print("  m, Bstart-snap, Bdot-done-snap, A-arrived-snap, publish-snap, deadline-snap")
+        for r in rows[:24]: print("   ", r)
+        late = [r for r in rows if r[4] > r[5]]; print('  late inits', len(late), 'of', len(rows))
