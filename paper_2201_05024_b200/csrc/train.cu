@@ -51,16 +51,17 @@ namespace kapsm {
 
 constexpr int TC_S = 32;                    // slots (one warp)
 constexpr int TC_BT = 4;                    // batch: takeover / entry / publication every 4 steps
-constexpr int TC_MAX_W = 24;                // lookahead D >= 4 with D + W <= 29
+constexpr int TC_MAX_W = 23;                // lookahead D = 8 with D + W <= 31
 constexpr int TC_PF = 2;                    // column prefetch distance (batches)
 constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2 > PF)
 constexpr int TC_INIT = 64;                 // init values (ring, pow2)
 constexpr int TC_Q = 61;                    // init: early part i <= m - Q, late part <= 32 elements
 constexpr int TC_MAX_NP = 3072;
-// slot reuse: the batch taken over after step n (samples n+D..n+D+3) reuses
-// the slots of samples that left the window by step n: D + 3 + W - 33 <= 0.
+// slot reuse: the batch taken over after step n+1 (samples n+D..n+D+3)
+// reuses the slots of samples that left the window by step n+1:
+// D + 3 + W - 33 <= 1.
 __host__ __device__ constexpr int lookahead(int wm) {
-  return ((30 - wm) & ~3) > 8 ? 8 : ((30 - wm) & ~3);
+  return ((31 - wm) & ~3) > 8 ? 8 : ((31 - wm) & ~3);
 }
 constexpr long long TC_SPIN_LIMIT = 1LL << 20;
 
@@ -613,41 +614,57 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
           if (!(FEAT & 8)) cp_async_wait<TC_PF - 1>();
         });
         mark(0);
+        // ---- step n+1 ----
+        step(n + 1, ic<(k0 + 1) & 31>{}, false, [&] {
+          if (!(FEAT & 32)) weights(n + 2, qcm[1], qcl[1]);
+          if (!(FEAT & 16)) init_load(n + TC_BT);
+        });
+        mark(1);
         if (!(FEAT & 1)) {
-          // ---- publish samples that left during steps n-3..n (c final) ----
-          if ((unsigned)(n - mleave) < (unsigned)TC_BT && m >= 0) {
+          // ---- publish samples that left during steps n-2..n+1 (c final) ----
+          if ((unsigned)(n + 1 - mleave) < (unsigned)TC_BT && m >= 0) {
             sts(cfa, c);
             st_tag(cta, c, m);
             if (CL > 1) st_tag_cl(bctag_s + (cta - ctag_s), c, m);
             sts_i(fsa, fs == 0x7fffffff ? -1 : fs);
           }
-          // ---- c^(n+1) of the slots that stay (the batch's slots give 0):
+          // ---- c^(n+2) of the slots that stay (the batch's slots give 0):
           //      the new samples' responses to them are formed in this warp ----
           sts(snap_s + ((jb & 1) * TC_S + x) * TS, isnew ? T(0) : c);
         }
         warp_sync_full();                                     // staged batch visible to all
-        mark(1);
-        // ---- step n+1: the new slots start from 0 with their staged columns
-        //      (loaded under the window loads); init of the next block's
-        //      entering samples is loaded too ----
+        // ---- takeover of the batch n+D .. n+D+3: the staged columns (the new
+        //      slots accumulate from step n+2; the loads land under its chain) ----
         T diag = T(0), bt = T(0);
-        step(n + 1, ic<(k0 + 1) & 31>{}, isnew, [&] {
-          if (!(FEAT & 2)) {
+        if (!(FEAT & 2)) {
 #pragma unroll
-            for (int i = 0; i < TC_BT; ++i)
-              row[(k0 + D + i) & (TC_S - 1)] = lds_t<T>(sb + (i * TC_S + x) * TS);
-            if (isnew) load_row32(sb + (rel & (TC_BT - 1)) * TC_S * TS, row);
-          }
-          if (!(FEAT & 4)) {
-            diag = lds_t<T>(sb + ((rel & (TC_BT - 1)) * TC_S + x) * TS);
-            bt = lds_nv(bsm_s + (unsigned)mt * TS, T(0));
-          }
-          if (!(FEAT & 16)) init_load(n + TC_BT);
-          // (zero for the taken-over slots with either their old or new state)
-          if (!(FEAT & 32)) weights(n + 2, qcm[1], qcl[1]);
-        });
-        mark(2);
+          for (int i = 0; i < TC_BT; ++i)
+            row[(k0 + D + i) & (TC_S - 1)] = lds_t<T>(sb + (i * TC_S + x) * TS);
+          if (isnew) load_row32(sb + (rel & (TC_BT - 1)) * TC_S * TS, row);
+        }
         if (!(FEAT & 4)) {
+          diag = lds_t<T>(sb + ((rel & (TC_BT - 1)) * TC_S + x) * TS);
+          bt = lds_nv(bsm_s + (unsigned)mt * TS, T(0));
+        }
+        mark(2);
+        // ---- step n+2: the new slots start from 0; entry check of the next
+        //      block's samples; the slot coefficients for the in-slot init ----
+        T cs[TC_S];
+        step(n + 2, ic<(k0 + 2) & 31>{}, isnew, [&] {
+          if (!(FEAT & 32)) weights(n + 3, qcm[2], qcl[2]);
+          if (!(FEAT & 16)) init_check(n + TC_BT);
+          if (!(FEAT & 2)) {
+            const unsigned csa = snap_s + (jb & 1) * TC_S * TS;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              T c4[4];
+              lds_quad<T>(csa + 4 * q * TS, c4);
+              cs[4 * q] = c4[0]; cs[4 * q + 1] = c4[1]; cs[4 * q + 2] = c4[2]; cs[4 * q + 3] = c4[3];
+            }
+          }
+        });
+        mark(3);
+        if (!(FEAT & 4)) {                                    // takeover state
           const bool v = mt < Np;
           const T inv = v ? recip(diag) : T(0);
           degen |= isnew && v && !(diag > T(0));
@@ -662,34 +679,9 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
           fsa = isnew ? fsfin_s + 4u * (unsigned)mt : fsa;
           cfa = isnew ? cfin_s + (unsigned)mt * TS : cfa;
         }
-        mark(3);
-        // ---- step n+2: entry check of the next block's samples, staging of a
-        //      later batch ----
-        // ---- step n+2: entry check of the next block's samples; the new
-        //      slots' response to the coefficients that stay in the slots
-        //      (sum_l c_l^(n+1) K[sample(l)][mt], the in-slot part of init_mt) ----
-        T yinit = T(0);
-        step(n + 2, ic<(k0 + 2) & 31>{}, false, [&] {
-          if (!(FEAT & 32)) weights(n + 3, qcm[2], qcl[2]);
-          if (!(FEAT & 16)) init_check(n + TC_BT);
-          if (!(FEAT & 2)) {
-            const unsigned cs = snap_s + (jb & 1) * TC_S * TS;
-            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              T c4[4];
-              lds_quad<T>(cs + 4 * q * TS, c4);
-              a0 = fma(c4[0], row[4 * q], a0);
-              a1 = fma(c4[1], row[4 * q + 1], a1);
-              a2 = fma(c4[2], row[4 * q + 2], a2);
-              a3 = fma(c4[3], row[4 * q + 3], a3);
-            }
-            yinit = (a0 + a1) + (a2 + a3);
-          }
-        });
-        if (isnew) { bme -= yinit; bpe -= yinit; bm -= yinit; bp -= yinit; }
         if (!(FEAT & 8)) stage_issue(jb + TC_PF);
-        mark(4);
+        // ---- step n+3; after it: the in-slot part of the new samples' init,
+        //      sum_l c_l^(n+2) K[sample(l)][mt], folded into their targets ----
         step(n + 3, ic<(k0 + 3) & 31>{}, false, [&] {
           if (!(FEAT & 32)) {
             weights(n + TC_BT, qcm[3], qcl[3]);
@@ -697,8 +689,21 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
             for (int i = 0; i < TC_BT; ++i) qload(n + TC_BT + 1 + i, qcm[i], qcl[i]);
           }
         });
+        mark(4);
+        if (!(FEAT & 2)) {
+          T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            a0 = fma(cs[4 * q], row[4 * q], a0);
+            a1 = fma(cs[4 * q + 1], row[4 * q + 1], a1);
+            a2 = fma(cs[4 * q + 2], row[4 * q + 2], a2);
+            a3 = fma(cs[4 * q + 3], row[4 * q + 3], a3);
+          }
+          const T yinit = (a0 + a1) + (a2 + a3);
+          if (isnew) { bme -= yinit; bpe -= yinit; bm -= yinit; bp -= yinit; }
+        }
         mark(5);
-        nlast = n;                                 // last publication point
+        nlast = n + 1;                             // last publication point
         return true;
       };
 
@@ -970,6 +975,7 @@ int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long 
   if (W <= 16) KAPSM_LT(16);
   if (W <= 20) KAPSM_LT(20);
   KAPSM_LT(TC_MAX_W);
+  static_assert(lookahead(TC_MAX_W) == 8, "the entry/takeover schedule assumes D = 8");
 #undef KAPSM_LT
 }
 
