@@ -55,6 +55,7 @@ constexpr int TC_MAX_W = 23;                // lookahead D = 8 with D + W <= 31
 constexpr int TC_PF = 2;                    // column prefetch distance (batches)
 constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2 > PF)
 constexpr int TC_INIT = 64;                 // init values (ring, pow2)
+constexpr int TC_ERING = 128;               // early init parts in flight (tagged ring, pow2)
 constexpr int TC_Q = 61;                    // init: early part i <= m - Q, late part <= 32 elements
 constexpr int TC_MAX_NP = 3072;
 // slot reuse: the batch taken over after step n+1 (samples n+D..n+D+3)
@@ -334,25 +335,31 @@ KAPSM_DEV double slot_value<double>(const Tagged<double>::slot_t& w) {
 //          w / 4 (3 = critical).
 template <int NG, int CL> struct Roles;
 // Every role: NB = id of the critical role; NA A workers, NBH B helpers.
-// Every role: NB = id of the critical role, NA init workers (ids 0..NA-1).
+// Roles: NB = id of the critical role; workers are early (kind 1: the early
+// init parts, far ahead of need) or late (kind 2: the short deadline path).
 template <> struct Roles<1, 2> {
-  static constexpr int NB = 8, NA = 8, ACH = 12, WARPS = 8;   // ACH: row vectors per lane
+  static constexpr int NE = 8, NL = 4, NB = NE + NL, ACH = 12, WARPS = 8;  // ACH: row vectors/lane
   static KAPSM_DEV int group(int) { return 0; }
-  // rank 0: warp 7 critical, warps 0..6 idle until the epilogue; rank 1: workers
-  static KAPSM_DEV int role(int w, unsigned rank) { return rank ? w : (w == 7 ? NB : -1); }
-  static KAPSM_DEV int a_index(int role) { return role; }
+  // rank 0: warp 7 critical; warps 0,1,2,4 late finishers (next to the
+  // critical warp: local latency; one per sample of a batch, off its
+  // sub-partition), warps 3,5,6 idle until the epilogue; rank 1: early workers
+  static KAPSM_DEV int role(int w, unsigned rank) {
+    if (rank) return w;
+    if (w == 7) return NB;
+    if (w < 3) return NE + w;
+    return w == 4 ? NE + 3 : -1;
+  }
 };
 template <> struct Roles<4, 1> {
-  static constexpr int NB = 3, NA = 3, ACH = 4, WARPS = 16;
+  static constexpr int NE = 2, NL = 1, NB = NE + NL, ACH = 4, WARPS = 16;
   static KAPSM_DEV int group(int w) { return w & 3; }
-  static KAPSM_DEV int role(int w, unsigned) { return w >> 2; }   // 0..2 workers, 3 critical
-  static KAPSM_DEV int a_index(int role) { return role; }
+  static KAPSM_DEV int role(int w, unsigned) { return w >> 2; }   // 0,1 early  2 late  3 critical
 };
 
 template <typename T, int NG, int CL>
 struct GroupSmem {
   // byte offsets of one group's region in dynamic shared memory
-  size_t dv, snap, stage, initr, ctag, cfin, fsfin, bsm, qsm, ctl, total;
+  size_t dv, snap, stage, initr, ering, ctag, cfin, fsfin, bsm, qsm, ctl, total;
   __host__ __device__ GroupSmem(int W, int Np) {
     using Slot = typename Tagged<T>::slot_t;
     constexpr int NB = Roles<NG, CL>::NB;
@@ -362,6 +369,7 @@ struct GroupSmem {
     snap = take((size_t)2 * TC_S * sizeof(T));   // slot coefficients after a block's 1st step
     stage = take((size_t)TC_SRING * TC_BT * TC_S * sizeof(T));
     initr = take((size_t)TC_INIT * sizeof(Slot));
+    ering = take((size_t)TC_ERING * sizeof(Slot));
     ctag = take((size_t)(Np + TC_S) * sizeof(Slot));
     cfin = take((size_t)(Np + TC_S) * sizeof(T));
     fsfin = take((size_t)(Np + TC_S) * sizeof(int));
@@ -454,6 +462,10 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
 
     // ---------------- per-task group state ----------------
     for (int i = gt; i < TC_INIT; i += GT) Tagged<T>::store(&initr[i], T(0), -1);
+    {
+      Slot* ering = reinterpret_cast<Slot*>(gs + L.ering);
+      for (int i = gt; i < TC_ERING; i += GT) Tagged<T>::store(&ering[i], T(0), -1);
+    }
     for (int i = gt; i < Np + TC_S; i += GT) { Tagged<T>::store(&ctag[i], T(0), -1); fsfin[i] = -1; }
     for (int i = gt; i < Np + 2 * TC_S; i += GT) bsm[i] = i < Np ? B[i] : T(0);
     for (int i = gt; i <= W; i += GT) {
@@ -738,51 +750,23 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       // over: its Gram row is streamed from L2 into registers, double
       // buffered) plus a late part over (m - Q, lastF] (one element per lane)
       // once c_lastF is published, and push it into the critical CTA's ring.
-      const int j = R::a_index(role);
-      constexpr int nw = R::NA;
+      // Early workers (NE warps) compute the early part far ahead into a local
+      // tagged ring; late finishers (NL warps) wait for c_lastF, add the late
+      // part and push init_m: the deadline path is short and never queued
+      // behind a long dot.
+      constexpr int NE = R::NE, NL = R::NL;
+      const bool early = role < NE;                        // roles 0..NE-1 early, NE.. late
+      const int j = early ? role : role - NE;
+      const int nw = early ? NE : NL;
       const unsigned gbase = smem_u32(gs);
-      const unsigned ctag_s = gbase + (unsigned)L.ctag;
-      const unsigned cinitr_s = cw_base + (unsigned)L.initr;   // the critical CTA's ring
+      const unsigned ctag_s = gbase + (unsigned)L.ctag, ering_s = gbase + (unsigned)L.ering;
+      const unsigned cinitr_s = cw_base + (unsigned)L.initr;   // the critical CTA's rings
+      const unsigned cering_s = cw_base + (unsigned)L.ering;
       auto mtask = [&](int t) { return FIRST + j + t * nw; };
       bool stop = false;
-      if (j == 0)                                          // f0 only before any update
+      if (early && j == 0)                                 // f0 only before any update
         for (int i = lane; i < FIRST && i < Np; i += 32)
           st_tag_cl(cinitr_s + (i & (TC_INIT - 1)) * SS, P0 ? P0[i] : T(0), i);
-      using V16 = typename Vec16<T>::type;                 // 16-byte vector of T
-      constexpr int EPV = 16 / sizeof(T);
-      constexpr int CH = 32 * EPV * ACH;                   // row elements per register chunk
-      V16 ra0[ACH], ra1[ACH];
-      T kl0 = T(0), kl1 = T(0);                            // late-part Gram entry per lane
-      auto a_issue = [&](V16 (&ra)[ACH], int mt, int lastA, int c0) {
-        const T* rowp = G + (long long)mt * ld;
-#pragma unroll
-        for (int u = 0; u < ACH; ++u) {
-          const int i = c0 + (u * 32 + lane) * EPV;
-          if (i <= lastA) ra[u] = ldg16(rowp + i);
-        }
-      };
-      // chunk c0 against the published final coefficients (tagged; a tag not
-      // yet visible makes the chunk redo)
-      auto a_dot = [&](const V16 (&ra)[ACH], int lastA, int c0) -> T {
-        for (;;) {
-          T acc0 = T(0), acc1 = T(0);
-          bool bad = false;
-#pragma unroll
-          for (int u = 0; u < ACH; ++u) {
-            const int i = c0 + (u * 32 + lane) * EPV;
-            if (i + EPV - 1 <= lastA) {
-              acc0 = tagged_dot16<T>(ctag_s + i * SS, i, ra[u], acc0, bad);
-            } else if (i <= lastA) {
-              for (int e = 0; e < EPV && i + e <= lastA; ++e) {
-                T cv;
-                bad |= !ld_tag(ctag_s + (i + e) * SS, i + e, cv);
-                acc1 = fma(cv, elem16(ra[u], e), acc1);
-              }
-            }
-          }
-          if (!__any_sync(0xffffffffu, bad)) return acc0 + acc1;
-        }
-      };
       auto wait_final = [&](int i) {                      // c_i published?
         T cl;
         long long spins = 0;
@@ -795,48 +779,119 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       // samples n_m+D-28 .. n_m; the taken-over slots' old samples and all
       // older ones are final by then
       auto lastf = [&](int mt) { return ((mt - D) & ~(TC_BT - 1)) + D - TC_S + TC_BT - 1; };
-      auto a_start = [&](V16 (&ra)[ACH], T& kl, int t) {
-        const int mt = mtask(t);
-        if (mt >= Np) return;
-        if (mt - TC_Q >= 0) a_issue(ra, mt, mt - TC_Q, 0);
-        const int i = mt - TC_Q + 1 + lane;                // late part: one element per lane
-        kl = (i >= 0 && i <= lastf(mt)) ? G[(long long)mt * ld + i] : T(0);
-      };
-      auto a_finish = [&](V16 (&ra)[ACH], T kl, int t) -> bool {
-        const int mt = mtask(t);
-        if (mt >= Np) return false;
-        const int lastA = mt - TC_Q, lastF = lastf(mt);
-        T part = T(0);
-        if (lastA >= 0) {                                  // early part
-          wait_final(lastA);
-          if (stop) return false;
-          part = a_dot(ra, lastA, 0);
-          for (int c0 = CH; c0 <= lastA; c0 += CH) {        // rows longer than one chunk
-            a_issue(ra, mt, lastA, c0);                     // (the consumed buffer is reused)
-            part += a_dot(ra, lastA, c0);
+      if (early) {
+        // ------------------------- early part: i <= m - Q -------------------------
+        using V16 = typename Vec16<T>::type;               // 16-byte vector of T
+        constexpr int EPV = 16 / sizeof(T);
+        constexpr int CH = 32 * EPV * ACH;                 // row elements per register chunk
+        V16 ra0[ACH], ra1[ACH];
+        auto a_issue = [&](V16 (&ra)[ACH], int mt, int lastA, int c0) {
+          const T* rowp = G + (long long)mt * ld;
+#pragma unroll
+          for (int u = 0; u < ACH; ++u) {
+            const int i = c0 + (u * 32 + lane) * EPV;
+            if (i <= lastA) ra[u] = ldg16(rowp + i);
           }
-        }
-        if (lastF >= 0) {                                  // late part
-          wait_final(lastF);
-          if (stop) return false;
-          const int i = mt - TC_Q + 1 + lane;
+        };
+        // chunk c0 against the published final coefficients (tagged; a tag not
+        // yet visible makes the chunk redo)
+        auto a_dot = [&](const V16 (&ra)[ACH], int lastA, int c0) -> T {
           for (;;) {
-            T cv = T(0);
+            T acc0 = T(0), acc1 = T(0);
             bool bad = false;
-            if (i >= 0 && i <= lastF) bad = !ld_tag(ctag_s + i * SS, i, cv);
-            if (!__any_sync(0xffffffffu, bad)) { part = fma(cv, kl, part); break; }
+#pragma unroll
+            for (int u = 0; u < ACH; ++u) {
+              const int i = c0 + (u * 32 + lane) * EPV;
+              if (i + EPV - 1 <= lastA) {
+                acc0 = tagged_dot16<T>(ctag_s + i * SS, i, ra[u], acc0, bad);
+              } else if (i <= lastA) {
+                for (int e = 0; e < EPV && i + e <= lastA; ++e) {
+                  T cv;
+                  bad |= !ld_tag(ctag_s + (i + e) * SS, i + e, cv);
+                  acc1 = fma(cv, elem16(ra[u], e), acc1);
+                }
+              }
+            }
+            if (!__any_sync(0xffffffffu, bad)) return acc0 + acc1;
           }
+        };
+        auto a_start = [&](V16 (&ra)[ACH], int t) {
+          const int mt = mtask(t);
+          if (mt < Np && mt - TC_Q >= 0) a_issue(ra, mt, mt - TC_Q, 0);
+        };
+        auto a_finish = [&](V16 (&ra)[ACH], int t) -> bool {
+          const int mt = mtask(t);
+          if (mt >= Np) return false;
+          const int lastA = mt - TC_Q;
+          T part = T(0);
+          if (lastA >= 0) {
+            wait_final(lastA);
+            if (stop) return false;
+            part = a_dot(ra, lastA, 0);
+            for (int c0 = CH; c0 <= lastA; c0 += CH) {      // rows longer than one chunk
+              a_issue(ra, mt, lastA, c0);                   // (the consumed buffer is reused)
+              part += a_dot(ra, lastA, c0);
+            }
+            part = warp_sum(part);
+          }
+          if (lane == 0) st_tag_cl(cering_s + (mt & (TC_ERING - 1)) * SS, part + (P0 ? P0[mt] : T(0)), mt);
+          return true;
+        };
+        a_start(ra0, 0);
+        for (int t = 0; !stop; t += 2) {                    // unrolled by 2: buffers swap
+          a_start(ra1, t + 1);
+          if (!a_finish(ra0, t)) break;
+          a_start(ra0, t + 2);
+          if (!a_finish(ra1, t + 1)) break;
         }
-        const T tot = warp_sum(part) + (P0 ? P0[mt] : T(0));
-        if (lane == 0) st_tag_cl(cinitr_s + (mt & (TC_INIT - 1)) * SS, tot, mt);
-        return true;
-      };
-      a_start(ra0, kl0, 0);
-      for (int t = 0; !stop; t += 2) {                      // unrolled by 2: buffers swap
-        a_start(ra1, kl1, t + 1);
-        if (!a_finish(ra0, kl0, t)) break;
-        a_start(ra0, kl0, t + 2);
-        if (!a_finish(ra1, kl1, t + 1)) break;
+      } else {
+        // ---------------- late part (m - Q, lastF], then publish ----------------
+        const unsigned initr_s_loc = gbase + (unsigned)L.initr;   // (the critical CTA)
+        auto l_load = [&](int t) -> T {                   // one Gram entry per lane
+          const int mt = mtask(t);
+          const int i = mt - TC_Q + 1 + lane;
+          return (mt < Np && i >= 0 && i <= lastf(mt)) ? G[(long long)mt * ld + i] : T(0);
+        };
+        auto l_task = [&](int t, T kl) -> bool {
+          const int mt = mtask(t);
+          if (mt >= Np) return false;
+          const int lastF = lastf(mt);
+          T part = T(0);
+          if (DBG && lane == 0 && fu == 0) dbg[3 * Np + mt] = clock64();
+          if (lastF >= 0) {
+            wait_final(lastF);
+            if (stop) return false;
+            if (DBG && lane == 0 && fu == 0) dbg[5 * Np + 1 + mt] = clock64();
+            const int i = mt - TC_Q + 1 + lane;
+            for (;;) {
+              T cv = T(0);
+              bool bad = false;
+              if (i >= 0 && i <= lastF) bad = !ld_tag(ctag_s + i * SS, i, cv);
+              if (!__any_sync(0xffffffffu, bad)) { part = cv * kl; break; }
+            }
+            part = warp_sum(part);
+          }
+          if (lane == 0) {
+            T e;
+            long long spins = 0;
+            while (!ld_tag(ering_s + (mt & (TC_ERING - 1)) * SS, mt, e))
+              if (((++spins) & 1023) == 0 && (spins > TC_SPIN_LIMIT || ld_volatile(&ctl[1]))) {
+                stop = true; red_or_cl(cw_base + (unsigned)L.ctl + 8u, 16);
+                break;
+              }
+            if (DBG && fu == 0) dbg[4 * Np + mt] = clock64();
+            st_tag(initr_s_loc + (mt & (TC_INIT - 1)) * SS, e + part, mt);
+          }
+          stop = __shfl_sync(0xffffffffu, stop, 0);
+          return !stop;
+        };
+        T kl0 = l_load(0), kl1;
+        for (int t = 0; !stop; t += 2) {                    // unrolled by 2: entries swap
+          kl1 = l_load(t + 1);
+          if (!l_task(t, kl0)) break;
+          kl0 = l_load(t + 2);
+          if (!l_task(t + 1, kl1)) break;
+        }
       }
       if (stop && lane == 0) raise_abort(KAPSM_TRAIN_STALLED);
     }

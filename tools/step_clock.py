@@ -41,10 +41,10 @@ for var in variants:
         rows = []
         for m in range(400, 560):
             nm = (m - D) & ~3
-            snapt = t[nm + 1] if nm + 1 < Np else 0
+            snapt = t[nm + 2] if nm + 2 < Np else 0
             dead = t[(m & ~3) - 2] if (m & ~3) - 2 < Np else 0
             bdone = allc[5*Np+1+m]
             rows.append((m, int(bst[m]-snapt), int(bdone-snapt), int(aend[m]-snapt), int(pub[m]-snapt), int(dead-snapt)))
-        print("  m, Bstart-snap, Bdot-done-snap, A-arrived-snap, publish-snap, deadline-snap")
+        print("  m (rel. to CW step n_m+2 start): task-start, lastF-seen, early-part-seen, -, deadline")
         for r in rows[:24]: print("   ", r)
         late = [r for r in rows if r[4] > r[5]]; print('  late inits', len(late), 'of', len(rows))
