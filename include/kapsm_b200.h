@@ -91,7 +91,9 @@ int kapsm_sample_gram_f64(const double* S, long long s_stride, int F, int N, int
  * three-case beta (apsm.py:185-191, 329-332), uniform weights
  * (apsm.py:139-153), theta update (apsm.py:338) and first-activation slot
  * bookkeeping (apsm.py:341-359), with no per-step launch.
- *   gram      : K1 output (kapsm_pilot_gram_* or kapsm_sample_gram_*).
+ *   gram      : K1 output (kapsm_pilot_gram_* or kapsm_sample_gram_*);
+ *               ld >= n_samples + 16 (16-byte aligned rows), and 32 x ld zero
+ *               elements must follow the last frame's matrix.
  *   sample source for the final theta, exactly one non-NULL:
  *     rx / rx_stride            complex pilots (n_samples = 2*n_train, dim = 2M)
  *     samples / samples_stride  realified rows F x n_samples x dim
@@ -195,7 +197,9 @@ int kapsm_count_mismatch(const void* a, const void* b, long long n, int elem_byt
 /* ---------------------------------------------------------------------------
  * Whole frame pipeline on one stream: zero the counters, K1, K2, K3 for all K
  * users of F frames (run_trial, noma.py:249-281, once per target user).
- * gram_ws: workspace F x (2*n_train) x ld, ld >= 2*n_train.  Other arguments as
+ * gram_ws: workspace F x (2*n_train) x ld, ld >= 2*n_train + 16, followed by
+ *          32 x ld zero elements (the trainer's staged reads run past the last
+ *          sample into them).  Other arguments as
  * for the three stages.  Captured into a CUDA graph by the host.
  * ------------------------------------------------------------------------- */
 int kapsm_run_frames_f32(const float* rx, long long rx_stride, const float* pilots,
@@ -214,6 +218,64 @@ int kapsm_run_frames_f64(const double* rx, long long rx_stride, const double* pi
                          int* first_step, double* theta, int* n_active, int* status, double* est,
                          unsigned char* labels, unsigned long long* bit_err,
                          unsigned long long* sym_err, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Split detection for the latency pipeline (csrc/screen.cu).
+ * kapsm_detect_screen_*: the pilot/payload kernel screen of F frames, which
+ *   does not depend on the filters (it can run concurrently with training).
+ *   live: workspace of kapsm_screen_workspace_bytes(F, n_train, n_data) bytes
+ *   (16-byte aligned); it starts with F x ceil(n_train/32) x n_data uint32
+ *   bits: bit p%32 of live[f][p/32][t] is set when some realified kernel of
+ *   (pilot p, payload t) does not underflow (the screen the fused kernel
+ *   applies per pair), followed by per-symbol compact lists of the live
+ *   pilots' kernel values.
+ * kapsm_detect_finish_*: the fused detection epilogue (linear part, the
+ *   Gaussian part over the live pilots recomputed with explicit differences,
+ *   demap, error counts) from the screen's live bits; other arguments as for
+ *   kapsm_detect_frames_*.
+ * ------------------------------------------------------------------------- */
+long long kapsm_screen_workspace_bytes(int F, int n_train, int n_data);
+int kapsm_detect_screen_f32(const float* rx, long long rx_stride, int F, int n_train, int n_data,
+                            int M, kapsm_kernel_params p, unsigned* live, void* stream);
+int kapsm_detect_screen_f64(const double* rx, long long rx_stride, int F, int n_train,
+                            int n_data, int M, kapsm_kernel_params p, unsigned* live,
+                            void* stream);
+int kapsm_detect_finish_f32(const float* rx, long long rx_stride, int F, int K, int n_train,
+                            int n_data, int M, const float* coeff, const float* theta,
+                            kapsm_kernel_params p, const float* points, int n_points,
+                            int bits_per_symbol, const unsigned char* tx_labels,
+                            const unsigned* live, float* est, unsigned char* labels,
+                            unsigned long long* bit_err, unsigned long long* sym_err,
+                            void* stream);
+int kapsm_detect_finish_f64(const double* rx, long long rx_stride, int F, int K, int n_train,
+                            int n_data, int M, const double* coeff, const double* theta,
+                            kapsm_kernel_params p, const double* points, int n_points,
+                            int bits_per_symbol, const unsigned char* tx_labels,
+                            const unsigned* live, double* est, unsigned char* labels,
+                            unsigned long long* bit_err, unsigned long long* sym_err,
+                            void* stream);
+
+/* Latency pipeline: kapsm_run_frames_* with the kernel screen on side_stream
+ * (fork/join through events, capturable into one CUDA graph) overlapping K1
+ * and K2, then the detection finish.  live_ws as for kapsm_detect_screen_*. */
+int kapsm_run_frames_overlap_f32(const float* rx, long long rx_stride, const float* pilots,
+                                 const unsigned char* tx_labels, int F, int K, int n_train,
+                                 int n_data, int M, int window, double epsilon,
+                                 kapsm_kernel_params p, const float* qtab, const float* points,
+                                 int n_points, int bits_per_symbol, float* gram_ws, long long ld,
+                                 unsigned* live_ws, float* coeff, int* first_step, float* theta,
+                                 int* n_active, int* status, float* est, unsigned char* labels,
+                                 unsigned long long* bit_err, unsigned long long* sym_err,
+                                 void* stream, void* side_stream);
+int kapsm_run_frames_overlap_f64(const double* rx, long long rx_stride, const double* pilots,
+                                 const unsigned char* tx_labels, int F, int K, int n_train,
+                                 int n_data, int M, int window, double epsilon,
+                                 kapsm_kernel_params p, const double* qtab, const double* points,
+                                 int n_points, int bits_per_symbol, double* gram_ws,
+                                 long long ld, unsigned* live_ws, double* coeff, int* first_step,
+                                 double* theta, int* n_active, int* status, double* est,
+                                 unsigned char* labels, unsigned long long* bit_err,
+                                 unsigned long long* sym_err, void* stream, void* side_stream);
 
 #ifdef __cplusplus
 }

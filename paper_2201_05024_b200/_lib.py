@@ -56,6 +56,19 @@ SIGNATURES = {
                                   _I, _P, _LL, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "kapsm_run_frames_f64": (_I, [_P, _LL, _P, _P, _I, _I, _I, _I, _I, _I, _D, _KP, _P, _P, _I,
                                   _I, _P, _LL, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "kapsm_screen_workspace_bytes": (_LL, [_I, _I, _I]),
+    "kapsm_detect_screen_f32": (_I, [_P, _LL, _I, _I, _I, _I, _KP, _P, _P]),
+    "kapsm_detect_screen_f64": (_I, [_P, _LL, _I, _I, _I, _I, _KP, _P, _P]),
+    "kapsm_detect_finish_f32": (_I, [_P, _LL, _I, _I, _I, _I, _I, _P, _P, _KP, _P, _I, _I, _P,
+                                     _P, _P, _P, _P, _P, _P]),
+    "kapsm_detect_finish_f64": (_I, [_P, _LL, _I, _I, _I, _I, _I, _P, _P, _KP, _P, _I, _I, _P,
+                                     _P, _P, _P, _P, _P, _P]),
+    "kapsm_run_frames_overlap_f32": (_I, [_P, _LL, _P, _P, _I, _I, _I, _I, _I, _I, _D, _KP, _P,
+                                          _P, _I, _I, _P, _LL, _P, _P, _P, _P, _P, _P, _P, _P,
+                                          _P, _P, _P, _P]),
+    "kapsm_run_frames_overlap_f64": (_I, [_P, _LL, _P, _P, _I, _I, _I, _I, _I, _I, _D, _KP, _P,
+                                          _P, _I, _I, _P, _LL, _P, _P, _P, _P, _P, _P, _P, _P,
+                                          _P, _P, _P, _P]),
     "kapsm_batch_evaluate_f32": (_I, [_P, _P, _P, _I, _I, _P, _I, _KP, _P, _P]),
     "kapsm_batch_evaluate_f64": (_I, [_P, _P, _P, _I, _I, _P, _I, _KP, _P, _P]),
     "kapsm_batch_detect_f32": (_I, [_P, _P, _P, _I, _I, _P, _I, _KP, _P, _P]),

@@ -10,11 +10,15 @@ template <> struct Fns<float> {
   static constexpr auto gram = kapsm_pilot_gram_f32;
   static constexpr auto train = kapsm_train_f32;
   static constexpr auto detect = kapsm_detect_frames_f32;
+  static constexpr auto screen = kapsm_detect_screen_f32;
+  static constexpr auto finish = kapsm_detect_finish_f32;
 };
 template <> struct Fns<double> {
   static constexpr auto gram = kapsm_pilot_gram_f64;
   static constexpr auto train = kapsm_train_f64;
   static constexpr auto detect = kapsm_detect_frames_f64;
+  static constexpr auto screen = kapsm_detect_screen_f64;
+  static constexpr auto finish = kapsm_detect_finish_f64;
 };
 
 template <typename T>
@@ -58,3 +62,74 @@ static int run_frames(const T* rx, long long rx_stride, const T* pilots,
   }
 KAPSM_RUN_ENTRY(kapsm_run_frames_f32, float)
 KAPSM_RUN_ENTRY(kapsm_run_frames_f64, double)
+
+// Latency pipeline: K3a (kernel screen, independent of the filters) runs on a
+// side stream while K1 -> K2 run on the main stream; K3b finishes once both
+// are done.  Stream-ordered fork/join through events, so it captures into one
+// CUDA graph.
+template <typename T>
+static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
+                              const unsigned char* tx_labels, int F, int K, int n_train,
+                              int n_data, int M, int window, double eps, kapsm_kernel_params p,
+                              const T* qtab, const T* points, int n_points, int bps, T* gram_ws,
+                              long long ld, unsigned* live_ws, T* coeff, int* first_step,
+                              T* theta, int* n_active, int* status, T* est,
+                              unsigned char* labels, unsigned long long* bit_err,
+                              unsigned long long* sym_err, void* stream, void* side_stream) {
+  cudaStream_t s = (cudaStream_t)stream, s2 = (cudaStream_t)side_stream;
+  if (F < 0 || K < 1 || n_train < 1 || n_data < 0 || M < 1 || !live_ws) return KAPSM_ERR_INVALID;
+  if (F == 0) return KAPSM_OK;
+  if (!s2 || s2 == s) return KAPSM_ERR_INVALID;
+  const int Np = 2 * n_train;
+  cudaEvent_t fork, join;
+  if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return KAPSM_ERR_CUDA;
+  if (cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaEventDestroy(fork);
+    return KAPSM_ERR_CUDA;
+  }
+  int r = KAPSM_OK;
+  do {
+    if (cudaEventRecord(fork, s) != cudaSuccess || cudaStreamWaitEvent(s2, fork, 0) != cudaSuccess) {
+      r = KAPSM_ERR_CUDA;
+      break;
+    }
+    if ((r = Fns<T>::screen(rx, rx_stride, F, n_train, n_data, M, p, live_ws, s2))) break;
+    if (cudaEventRecord(join, s2) != cudaSuccess) { r = KAPSM_ERR_CUDA; break; }
+    const long long gstride = (long long)Np * ld;
+    if ((r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream))) break;
+    if ((r = Fns<T>::train(gram_ws, ld, gstride, rx, rx_stride, nullptr, 0, 2 * M, pilots, F, K,
+                           Np, window, eps, p, qtab, nullptr, nullptr, coeff, first_step, theta,
+                           n_active, status, stream)))
+      break;
+    if (bit_err && cudaMemsetAsync(bit_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess) {
+      r = KAPSM_ERR_CUDA;
+      break;
+    }
+    if (sym_err && cudaMemsetAsync(sym_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess) {
+      r = KAPSM_ERR_CUDA;
+      break;
+    }
+    if (cudaStreamWaitEvent(s, join, 0) != cudaSuccess) { r = KAPSM_ERR_CUDA; break; }
+    r = Fns<T>::finish(rx, rx_stride, F, K, n_train, n_data, M, coeff, theta, p, points, n_points,
+                       bps, tx_labels, live_ws, est, labels, bit_err, sym_err, stream);
+  } while (false);
+  cudaEventDestroy(fork);
+  cudaEventDestroy(join);
+  return r;
+}
+
+#define KAPSM_RUN2_ENTRY(NAME, T)                                                              \
+  extern "C" int NAME(const T* rx, long long rx_stride, const T* pilots,                       \
+                      const unsigned char* tx_labels, int F, int K, int n_train, int n_data,   \
+                      int M, int window, double eps, kapsm_kernel_params p, const T* qtab,     \
+                      const T* points, int n_points, int bps, T* gram_ws, long long ld,        \
+                      unsigned* live_ws, T* coeff, int* first_step, T* theta, int* n_active,   \
+                      int* status, T* est, unsigned char* labels, unsigned long long* bit_err, \
+                      unsigned long long* sym_err, void* stream, void* side_stream) {          \
+    return run_frames_overlap<T>(rx, rx_stride, pilots, tx_labels, F, K, n_train, n_data, M,   \
+                                 window, eps, p, qtab, points, n_points, bps, gram_ws, ld,     \
+                                 live_ws, coeff, first_step, theta, n_active, status, est,     \
+                                 labels, bit_err, sym_err, stream, side_stream);               \
+  }
+KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f32, float)
+KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f64, double)

@@ -978,8 +978,9 @@ int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long lo
   }
   const GroupSmem<T, NG, CL> L(W, Np);
   size_t smem = L.total * NG;
-  // NG = 1: pad shared memory so that only one CTA fits per SM (the two CTAs
-  // of a cluster land on different SMs)
+  // NG = 1: pad shared memory so that the two CTAs of a cluster land on
+  // different SMs (the latency pipeline's concurrent detection screen asks
+  // for more than the rest of an SM, so it cannot share them either)
   if (NG == 1 && smem < 120 * 1024) smem = 120 * 1024;
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

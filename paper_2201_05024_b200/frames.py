@@ -13,6 +13,7 @@ tx labels (F, K, n_data) uint8; Gram workspace (F, Np, ld).
 
 from __future__ import annotations
 
+import ctypes as C
 from typing import Optional
 
 import numpy as np
@@ -36,7 +37,7 @@ def _ld(n: int) -> int:
 class FramePipeline:
     def __init__(self, F: int, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32",
-                 store_est: bool = True, device=None):
+                 store_est: bool = True, device=None, overlap: bool = True):
         if precision not in dv.DTYPES:
             raise ValueError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.cfg = cfg or ApsmConfig()
@@ -74,7 +75,18 @@ class FramePipeline:
         self.qtab = qtab_device(self.cfg.window, precision)
         self.points = points_device(scheme, precision)
         self.graph = None
-        self._fn = dv.fn("kapsm_run_frames", precision)
+        # latency pipeline: the detection kernel screen (independent of the
+        # filters) runs on a side stream, overlapping the Gram and the trainer
+        self.overlap = overlap
+        if overlap:
+            nbytes = int(lib.kapsm_screen_workspace_bytes(F, n_train, n_data))
+            self.live = torch.zeros(((nbytes + 15) // 16 * 4,), dtype=torch.int32, device=dev)
+            self._side = torch.cuda.Stream(device=dev)
+            self._fn = dv.fn("kapsm_run_frames_overlap", precision)
+        else:
+            self.live = None
+            self._side = None
+            self._fn = dv.fn("kapsm_run_frames", precision)
 
     # -- inputs -------------------------------------------------------------
     def load(self, rx, pilots, tx_labels, non_blocking: bool = False):
@@ -95,19 +107,26 @@ class FramePipeline:
     # -- compute ------------------------------------------------------------
     def _args(self):
         c = self.cfg
-        return (dv.ptr(self.rx), self.T * self.M * 2, dv.ptr(self.pilots), dv.ptr(self.tx),
+        head = (dv.ptr(self.rx), self.T * self.M * 2, dv.ptr(self.pilots), dv.ptr(self.tx),
                 self.F, self.K, self.n_train, self.n_data, self.M, c.window, float(c.epsilon),
                 _lib.params(c.params), dv.ptr(self.qtab), dv.ptr(self.points), self.n_points,
-                self.bps, dv.ptr(self.gram), self.ld, dv.ptr(self.coeff),
-                dv.ptr(self.first_step), dv.ptr(self.theta), dv.ptr(self.n_active),
-                dv.ptr(self.status), dv.ptr(self.est), dv.ptr(self.labels),
-                dv.ptr(self.bit_err), dv.ptr(self.sym_err))
+                self.bps, dv.ptr(self.gram), self.ld)
+        tail = (dv.ptr(self.coeff), dv.ptr(self.first_step), dv.ptr(self.theta),
+                dv.ptr(self.n_active), dv.ptr(self.status), dv.ptr(self.est),
+                dv.ptr(self.labels), dv.ptr(self.bit_err), dv.ptr(self.sym_err))
+        if self.overlap:
+            return head + (dv.ptr(self.live),) + tail
+        return head + tail
 
     def launch(self, time_detect: bool = False):
         """Enqueue the whole pipeline on the current stream.  With time_detect,
         run the stages separately and return the detection kernel time in us."""
         if not time_detect:
-            _lib.check(self._fn(*self._args(), dv.stream()), "run_frames")
+            if self.overlap:
+                _lib.check(self._fn(*self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
+                           "run_frames_overlap")
+            else:
+                _lib.check(self._fn(*self._args(), dv.stream()), "run_frames")
             return None
         lib = _lib.load()
         c = self.cfg

@@ -28,3 +28,17 @@ for name, fn in [("pilot_gram", gram), ("apsm_train", train), ("detect_frames", 
         ts.append(e0.elapsed_time(e1) * 1e3)
     print(f"{name:14s} F={F}: median {np.median(ts):8.1f} us  min {min(ts):8.1f} us")
 print("status", pipe.status.cpu().numpy().ravel()[:12].tolist(), "bit errors", int(pipe.bit_err.sum()))
+# split detection stages
+live = torch.zeros((int(_lib.load().kapsm_screen_workspace_bytes(F, pipe.n_train, pipe.n_data)) // 4 + 4,), dtype=torch.int32, device="cuda")
+def screen():
+    _lib.check(dv.fn("kapsm_detect_screen", "f32")(dv.ptr(pipe.rx), pipe.T * pipe.M * 2, pipe.F, pipe.n_train, pipe.n_data, pipe.M, p, dv.ptr(live), st), "s")
+def finish():
+    _lib.check(dv.fn("kapsm_detect_finish", "f32")(dv.ptr(pipe.rx), pipe.T * pipe.M * 2, pipe.F, pipe.K, pipe.n_train, pipe.n_data, pipe.M, dv.ptr(pipe.coeff), dv.ptr(pipe.theta), p, dv.ptr(pipe.points), pipe.n_points, pipe.bps, dv.ptr(pipe.tx), dv.ptr(live), dv.ptr(pipe.est), dv.ptr(pipe.labels), dv.ptr(pipe.bit_err), dv.ptr(pipe.sym_err), st), "f")
+for name, fn in [("detect_screen", screen), ("detect_finish", finish)]:
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); fn(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    print(f"{name:14s} F={F}: median {np.median(ts):8.1f} us  min {min(ts):8.1f} us")
+print("live bits set", int(torch.bitwise_count(live).sum()) if hasattr(torch, "bitwise_count") else "?")
