@@ -225,6 +225,71 @@ def test_multiframe_batch_equals_single():
         assert np.array_equal(one["bit_err"][0], full["bit_err"][i])
 
 
+def test_throughput_mode_many_tasks_per_group():
+    """F*K > 4 x SMs: throughput mode (4 chains per SM) with several tasks per
+    chain group (barriers re-armed between tasks).  Same decisions as the
+    latency mode (a 2-CTA cluster per chain) frame by frame; soft estimates
+    within the FP32 tolerance (the init dots are split differently)."""
+    F, Kn, M, nt, nd = 110, 6, 4, 40, 48
+    rx, pil, tx, _ = K.host_frames(list(range(300, 300 + F)), Kn, M, nt, nd, "QPSK")
+    pipe = K.FramePipeline(F, Kn, M, nt, nd, "QPSK", precision="f32")
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    full = pipe.results()
+    assert not full["status"].any()
+    for i in (0, 57, F - 1):
+        p1 = K.FramePipeline(1, Kn, M, nt, nd, "QPSK", precision="f32")
+        p1.load(rx[i:i + 1], pil[i:i + 1], tx[i:i + 1])
+        p1.launch()
+        one = p1.results()
+        assert np.array_equal(one["n_active"][0], full["n_active"][i])
+        assert np.array_equal(one["labels"][0], full["labels"][i])
+        assert np.array_equal(one["bit_err"][0], full["bit_err"][i])
+        assert maxrel(full["est"][i], one["est"][0]) <= 1e-4
+
+
+@pytest.mark.parametrize("prec,tol", [("f32", 1e-5), ("f64", 1e-12)])
+def test_overlap_pipeline_matches_fused(prec, tol):
+    """The latency pipeline (screen on a side stream + finish) against the
+    fused single-stream detection: same decisions and counts; the finish
+    recomputes live kernels with explicit differences (FP32: within 1e-5)."""
+    seeds = [11, 12]
+    rx, pil, tx, _ = K.host_frames(seeds, 6, 16, 120, 256, "QPSK")
+    out = []
+    for ov in (False, True):
+        pipe = K.FramePipeline(2, 6, 16, 120, 256, "QPSK", precision=prec, overlap=ov)
+        pipe.load(rx, pil, tx)
+        pipe.capture()
+        pipe.replay()
+        out.append(pipe.results())
+    a, b = out
+    assert np.array_equal(a["labels"], b["labels"])
+    assert np.array_equal(a["bit_err"], b["bit_err"]) and np.array_equal(a["sym_err"], b["sym_err"])
+    assert maxrel(b["est"], a["est"]) <= tol
+
+
+def test_window_limits():
+    """W up to kapsm_max_window() (23) trains; larger windows are refused."""
+    from paper_2201_05024_b200 import _lib
+    wmax = _lib.load().kapsm_max_window()
+    assert wmax >= 20
+    rng = np.random.default_rng(3)
+    T, M = 50, 4
+    rxp = (rng.standard_normal((T, M)) + 1j * rng.standard_normal((T, M))) / np.sqrt(2)
+    sym = (rng.choice([-1, 1], T) + 1j * rng.choice([-1, 1], T)) / np.sqrt(2)
+    stream = list(zip(rxp, sym))
+    R = O.realify(rxp)
+    B = O.realify_targets(sym)
+    for W in (wmax, 7):
+        f = K.train(None, stream, K.ApsmConfig(window=W), precision="f64")
+        ref = O.train_user(R, B, W=W)
+        assert f.n_atoms == ref["n_atoms"]
+        assert np.array_equal(f.atoms, ref["atoms"])
+        assert maxrel(f.coeffs, ref["coeffs"]) <= 1e-9
+    with pytest.raises(NotImplementedError):
+        K.train(None, stream, K.ApsmConfig(window=wmax + 1), precision="f64")
+
+
 # --------------------------------------------------------------------------- engine API
 def test_engine_golden_random_filter():
     g = np.load(os.path.join(GOLDEN, "engine_random.npz"))
