@@ -54,7 +54,9 @@ const char* kapsm_strerror(int code);
 int kapsm_abi_version(void);
 /* Largest APSM window W supported by kapsm_train_* in this build. */
 int kapsm_max_window(void);
-/* Largest number of realified training samples per (frame, user). */
+/* Upper bound on realified training samples per (frame, user); the
+ * trainer's shared-memory footprint (the final-coefficient array, n_samples
+ * words per chain) sets the effective limit: KAPSM_ERR_UNSUPPORTED beyond. */
 int kapsm_max_samples(void);
 
 /* ---------------------------------------------------------------------------
@@ -115,6 +117,9 @@ int kapsm_sample_gram_f64(const double* S, long long s_stride, int F, int N, int
  *   n_active  : x 1          number of activated samples (new atoms)
  *   status    : x 1          KAPSM_TRAIN_* flags
  * Limits: window <= kapsm_max_window(), n_samples <= kapsm_max_samples().
+ * window <= 23 and n_samples <= 3072 run the latency-scheduled trainer (one
+ * critical warp per chain); larger configurations run the general trainer
+ * (train_wide.cu: one CTA per chain, the Gram band in shared memory).
  * ------------------------------------------------------------------------- */
 int kapsm_train_f32(const float* gram, long long ld, long long gram_stride, const float* rx,
                     long long rx_stride, const float* samples, long long samples_stride, int dim,

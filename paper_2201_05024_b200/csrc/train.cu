@@ -1035,6 +1035,16 @@ int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long 
 #undef KAPSM_LT
 }
 
+// the general trainer (train_wide.cu) for windows / pilot counts beyond the
+// latency kernel's schedule
+template <typename T>
+int train_wide(const T* gram, long long ld, long long gram_stride, const T* rx,
+               long long rx_stride, const T* samples, long long samples_stride, int dim,
+               const T* targets, int F, int K, int Np, int W, double eps, kapsm_kernel_params p,
+               const T* qtab, const T* base0, const T* theta0, T* coeff, int* first_step,
+               T* theta, int* n_active, int* status, cudaStream_t s);
+int train_wide_max_window();
+
 template <typename T>
 int train(const T* gram, long long ld, long long gram_stride, const T* rx, long long rx_stride,
           const T* samples, long long samples_stride, int dim, const T* targets, int F, int K,
@@ -1047,12 +1057,18 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
     return KAPSM_ERR_INVALID;
   if ((rx == nullptr) == (samples == nullptr)) return KAPSM_ERR_INVALID;  // exactly one source
   if (rx && ((Np & 1) || (dim & 1))) return KAPSM_ERR_INVALID;
-  if (W > TC_MAX_W || Np > TC_MAX_NP) return KAPSM_ERR_UNSUPPORTED;
   // rows: 16-byte aligned with >= 16 padding columns (kapsm_b200.h)
   if (ld < Np + 16 || (ld * (long long)sizeof(T)) % 16 ||
       (gram_stride * (long long)sizeof(T)) % 16 || ((size_t)gram & 15))
     return KAPSM_ERR_INVALID;
   const int tasks = F * K;
+  // KAPSM_FORCE_WIDE (tests): the general trainer at any size
+  if (W > TC_MAX_W || Np > TC_MAX_NP || getenv("KAPSM_FORCE_WIDE")) {
+    if (dbg) return KAPSM_ERR_UNSUPPORTED;
+    return train_wide<T>(gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim,
+                         targets, F, K, Np, W, eps, p, qtab, base0, theta0, coeff, first_step,
+                         theta, n_active, status, s);
+  }
   // latency mode (a 2-CTA cluster per chain) while the chains fit twice on the
   // SMs; throughput mode (4 chains per SM) beyond.  FP64 (the parity/test
   // precision) always runs in latency mode.
@@ -1076,9 +1092,10 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
 
 }  // namespace kapsm
 
-extern "C" int kapsm_max_window(void) { return kapsm::TC_MAX_W; }
+extern "C" int kapsm_max_window(void) { return kapsm::train_wide_max_window(); }
 
-extern "C" int kapsm_max_samples(void) { return kapsm::TC_MAX_NP; }
+// beyond this the shared-memory footprint decides (KAPSM_ERR_UNSUPPORTED)
+extern "C" int kapsm_max_samples(void) { return 1 << 20; }
 
 #define KAPSM_TRAIN_ENTRY(NAME, T)                                                             \
   extern "C" int NAME(const T* gram, long long ld, long long gram_stride, const T* rx,         \
