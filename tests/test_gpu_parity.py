@@ -269,7 +269,7 @@ def test_overlap_pipeline_matches_fused(prec, tol):
 
 
 def test_window_limits():
-    """W up to kapsm_max_window() (23) trains; larger windows are refused."""
+    """W up to kapsm_max_window() trains (the general trainer beyond 23); larger windows are refused."""
     from paper_2201_05024_b200 import _lib
     wmax = _lib.load().kapsm_max_window()
     assert wmax >= 20

@@ -84,9 +84,13 @@ def test_wide_generic_stream_and_warm_start(force_wide):
 
 
 @pytest.mark.parametrize("W,n_train,M", [(24, 300, 16), (64, 685, 16), (128, 400, 16),
-                                         (146, 300, 8), (37, 200, 64)])
+                                         (-1, 300, 8), (37, 200, 64)])
 def test_wide_window_sweep_f64(W, n_train, M):
     """C3 window sweep rows (W in {64, 128} + the limits) against the oracle."""
+    if W < 0:
+        from paper_2201_05024_b200 import _lib
+        W = _lib.load().kapsm_max_window()
+        assert W >= 128
     fr = O.make_frame(W, 6, M, n_train, 8, "QPSK")
     R = O.realify(fr["rx"][:n_train])
     for u in (0, 5):

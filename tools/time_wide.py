@@ -40,3 +40,7 @@ for nt, W in pts:
     print(f"n_train {nt:5d} W {W:3d}: gram {res['gram']:9.1f} us  train {res['train']:10.1f} us "
           f"({res['train'] / p.Np * 1e3:7.1f} ns/step)  atoms {p.n_active.cpu().numpy().ravel().tolist()} "
           f"status {int(st_.max())}", flush=True)
+    if os.environ.get("WIDE_CLOCKS"):
+        fsv = p.first_step.cpu().numpy()[0, 0, 100:356].reshape(64, 4)
+        print("  phase clocks (cumulative from step start: pre-barrier, barrier, update, end):")
+        print("  median", np.median(fsv, axis=0).tolist(), " rows 10-14:", fsv[10:15].tolist())
