@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--throughput-frames", type=int, default=296)
     ap.add_argument("--cpu-frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the single-frame latency of the other BASELINE configs (C3/C4)")
     return ap.parse_args()
 
 
@@ -185,6 +187,49 @@ def cpu_cores():
 
 
 # ---------------------------------------------------------------------------
+OTHER_CONFIGS = {
+    # configs[2]: dictionary / window sweep points; configs[3]: massive MIMO
+    "C3_n2048_W64": dict(K=6, M=16, n_train=2048, n_data=3840, scheme="QPSK", W=64),
+    "C3_n8192_W128": dict(K=6, M=16, n_train=8192, n_data=3840, scheme="QPSK", W=128),
+    "C4_paper_frame": dict(K=16, M=64, n_train=685, n_data=3840, scheme="QAM16", W=20),
+    "C4_full_band": dict(K=16, M=64, n_train=6000, n_data=32400, scheme="QAM16", W=20),
+}
+
+
+def other_configs():
+    """Single-frame train+detect latency (CUDA graph replay, inputs resident)
+    of BASELINE.json's other configs, one seeded frame each, FP32."""
+    import numpy as np
+    import torch
+    import paper_2201_05024_b200 as K
+    out = {}
+    for name, c in OTHER_CONFIGS.items():
+        rx, pil, tx, _ = K.host_frames([3], c["K"], c["M"], c["n_train"], c["n_data"],
+                                       c["scheme"])
+        p = K.FramePipeline(1, c["K"], c["M"], c["n_train"], c["n_data"], c["scheme"],
+                            cfg=K.ApsmConfig(window=c["W"]), precision="f32", store_est=False)
+        p.load(rx, pil, tx)
+        p.capture()
+        p.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10 if c["n_train"] <= 2048 else 3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            p.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        nb = c["n_data"] * (2 if c["scheme"] == "QPSK" else 4) * c["K"]
+        out[name] = {"K": c["K"], "M": c["M"], "n_train": c["n_train"], "n_data": c["n_data"],
+                     "scheme": c["scheme"], "window": c["W"],
+                     "latency_us_p50": float(np.median(ts)), "reps": len(ts),
+                     "ber": int(p.bit_err.sum().item()) / nb, "status": int(p.status.max().item())}
+        del p
+        torch.cuda.empty_cache()
+    return out
+
+
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -465,6 +510,11 @@ def main():
                "latency_us_single_process": float(np.sum(ttimes) / args.cpu_frames * 1e6),
                "bit_errors": int(cerr)}
 
+    # ---------------- the other BASELINE configs (rank 0, N = 1) ----------------
+    others = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        others = other_configs()
+
     if rank == 0:
         launches_per_step = 4      # detect_screen, pilot_gram, apsm_train, detect_finish
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -487,6 +537,7 @@ def main():
               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                       "d2h_bytes_per_step": int(d2h)},
               "throughput_mode": thr,
+              "other_configs": others,
               "gpu_launches": launches_per_step * args.steps,
               "bit_errors_last_step": bit_err_last,
               "clocks": clk})
