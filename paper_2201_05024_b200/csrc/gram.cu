@@ -8,8 +8,11 @@
 //   ||r1(x)-r2(y)|| = ||x+iy||,  ||r2(x)-r1(y)|| = ||x-iy||.
 // Distances use explicit differences (kernels.py:187-191), never the
 // ||a||^2+||b||^2-2ab expansion, so near-coincident pilots keep full
-// precision.  Every sum is formed in an order that makes the matrix exactly
-// symmetric (thread (q,p) reproduces thread (p,q)'s transpose bit for bit).
+// precision.  Only the upper-triangular tiles are computed; off-diagonal tiles
+// also store their transpose (staged through shared memory), and inside a
+// diagonal tile every sum is formed in an order that makes thread (q,p)
+// reproduce thread (p,q)'s transpose bit for bit: the matrix is exactly
+// symmetric.
 #include "kapsm_common.cuh"
 
 namespace kapsm {
@@ -27,7 +30,14 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
   T* xb = xa + GRAM_TILE * rs;                   // [GRAM_TILE][rs]
   const int f = blockIdx.z;
   const T* X = rx + (long long)f * rx_stride;
-  const int p0 = blockIdx.y * GRAM_TILE, q0 = blockIdx.x * GRAM_TILE;
+  // upper-triangular tile grid: linear index -> (tile row ty <= tile column tx);
+  // off-diagonal tiles also write their transpose (the matrix is symmetric)
+  const int nt = (n_train + GRAM_TILE - 1) / GRAM_TILE;
+  int tr = 0, rem = (int)blockIdx.x;
+  while (rem >= nt - tr) { rem -= nt - tr; ++tr; }
+  const int tcol = tr + rem;
+  const int p0 = tr * GRAM_TILE, q0 = tcol * GRAM_TILE;
+  const bool offdiag = tcol != tr;
   const int tid = threadIdx.y * GRAM_TILE + threadIdx.x;
   const int row_elems = 2 * M;
   for (int e = tid; e < GRAM_TILE * row_elems; e += GRAM_TILE * GRAM_TILE) {
@@ -37,7 +47,7 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
   }
   __syncthreads();
   const int p = p0 + threadIdx.y, q = q0 + threadIdx.x;
-  if (p >= n_train || q >= n_train) return;
+  const bool inb = p < n_train && q < n_train;
   const T* x = xa + threadIdx.y * rs;
   const T* y = xb + threadIdx.x * rs;
   T s_rr = 0, s_ii = 0, s_ri = 0, s_ir = 0, nx = 0, ny = 0;
@@ -93,11 +103,31 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
   const T k21 = w_l * lin_21 + w_g * g_c;
   using V2 = typename Vec2<T>::type;
   T* G = gram + (long long)f * gram_stride;
-  V2 top, bot;
-  top.x = k11; top.y = k12;
-  bot.x = k21; bot.y = k11;
-  *reinterpret_cast<V2*>(G + (long long)(2 * p) * ld + 2 * q) = top;
-  *reinterpret_cast<V2*>(G + (long long)(2 * p + 1) * ld + 2 * q) = bot;
+  if (inb) {
+    V2 top, bot;
+    top.x = k11; top.y = k12;
+    bot.x = k21; bot.y = k11;
+    *reinterpret_cast<V2*>(G + (long long)(2 * p) * ld + 2 * q) = top;
+    *reinterpret_cast<V2*>(G + (long long)(2 * p + 1) * ld + 2 * q) = bot;
+  }
+  if (!offdiag) return;
+  // transposed block B(q,p) = B(p,q)^T through shared memory (coalesced rows)
+  __syncthreads();                               // the staged pilots are no longer read
+  constexpr int RT = 2 * GRAM_TILE;              // realified tile edge
+  T* tb = reinterpret_cast<T*>(smem_raw);        // [RT][RT + 1]
+  {
+    const int lp = 2 * threadIdx.y, lq = 2 * threadIdx.x;
+    tb[lq * (RT + 1) + lp] = k11;                // row 2q:   (k11, k21)
+    tb[lq * (RT + 1) + lp + 1] = k21;
+    tb[(lq + 1) * (RT + 1) + lp] = k12;          // row 2q+1: (k12, k11)
+    tb[(lq + 1) * (RT + 1) + lp + 1] = k11;
+  }
+  __syncthreads();
+  for (int e = tid; e < RT * RT; e += GRAM_TILE * GRAM_TILE) {
+    const int r = e / RT, c = e % RT;
+    const int gr = 2 * q0 + r, gc = 2 * p0 + c;
+    if (gr < 2 * n_train && gc < 2 * n_train) G[(long long)gr * ld + gc] = tb[r * (RT + 1) + c];
+  }
 }
 
 template <typename T>
@@ -108,8 +138,10 @@ int pilot_gram(const T* rx, long long rx_stride, int F, int n_train, int M,
     return KAPSM_ERR_INVALID;
   if (F == 0 || n_train == 0) return KAPSM_OK;
   const int nt = (n_train + GRAM_TILE - 1) / GRAM_TILE;
-  dim3 grid(nt, nt, F), block(GRAM_TILE, GRAM_TILE);
+  dim3 grid(nt * (nt + 1) / 2, 1, F), block(GRAM_TILE, GRAM_TILE);
   size_t smem = 2 * GRAM_TILE * (2 * (size_t)M + 1) * sizeof(T);
+  const size_t tsm = (size_t)(2 * GRAM_TILE) * (2 * GRAM_TILE + 1) * sizeof(T);
+  if (smem < tsm) smem = tsm;
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(pilot_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)

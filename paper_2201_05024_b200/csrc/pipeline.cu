@@ -63,9 +63,9 @@ static int run_frames(const T* rx, long long rx_stride, const T* pilots,
 KAPSM_RUN_ENTRY(kapsm_run_frames_f32, float)
 KAPSM_RUN_ENTRY(kapsm_run_frames_f64, double)
 
-// Latency pipeline: K3a (kernel screen, independent of the filters) runs on a
-// side stream while K1 -> K2 run on the main stream; K3b finishes once both
-// are done.  Stream-ordered fork/join through events, so it captures into one
+// Latency pipeline: K1 first, then K3a (kernel screen, independent of the
+// filters) on a side stream while K2 runs on the main stream; K3b finishes
+// once both are done.  Stream-ordered fork/join through events, so it captures into one
 // CUDA graph.
 template <typename T>
 static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
@@ -89,14 +89,16 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
   }
   int r = KAPSM_OK;
   do {
+    const long long gstride = (long long)Np * ld;
+    if ((r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream))) break;
+    // fork after K1: the screen then shares the GPU only with the trainer's
+    // few SMs instead of slowing the Gram down
     if (cudaEventRecord(fork, s) != cudaSuccess || cudaStreamWaitEvent(s2, fork, 0) != cudaSuccess) {
       r = KAPSM_ERR_CUDA;
       break;
     }
     if ((r = Fns<T>::screen(rx, rx_stride, F, n_train, n_data, M, p, live_ws, s2))) break;
     if (cudaEventRecord(join, s2) != cudaSuccess) { r = KAPSM_ERR_CUDA; break; }
-    const long long gstride = (long long)Np * ld;
-    if ((r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream))) break;
     if ((r = Fns<T>::train(gram_ws, ld, gstride, rx, rx_stride, nullptr, 0, 2 * M, pilots, F, K,
                            Np, window, eps, p, qtab, nullptr, nullptr, coeff, first_step, theta,
                            n_active, status, stream)))
