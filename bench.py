@@ -328,15 +328,21 @@ def main():
 
     lab_g = None
 
-    def step(i):
-        j = i % P
-        pipe.rx.copy_(rx_d[j:j + 1], non_blocking=True)
-        pipe.pilots.copy_(pil_d[j:j + 1], non_blocking=True)
-        pipe.tx.copy_(tx_d[j:j + 1], non_blocking=True)
-        pipe.replay()
+    def post(pp):
         if world > 1:
-            D.gather_decisions(pipe.labels)
-            D.reduce_counts(pipe.bit_err)
+            D.gather_decisions(pp.labels)
+            D.reduce_counts(pp.bit_err)
+
+    # device-resident steps: the pool frame is copied into one of two captured
+    # pipelines on a copy stream while the previous frame computes (FrameStream)
+    fs_dev = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32", depth=2,
+                           post=post)
+    last_ticket = [0]
+
+    def step(i, start=None):
+        j = i % P
+        last_ticket[0] = fs_dev.submit(rx_d[j:j + 1], pil_d[j:j + 1], tx_d[j:j + 1],
+                                       start_event=start)
 
     # ---------------- timed region: exactly K steps ----------------
     for i in range(args.warmup):
@@ -353,8 +359,10 @@ def main():
     e_all0.record()
     for i in range(args.steps):
         ev[i][0].record()
-        step(args.warmup + i)
+        step(args.warmup + i, start=e_all0 if i == 0 else None)
         ev[i][1].record()
+    cur = torch.cuda.current_stream()
+    cur.wait_event(fs_dev.done_event(last_ticket[0]))
     e_all1.record()
     torch.cuda.synchronize()
     barrier()
@@ -363,7 +371,8 @@ def main():
     step_us = np.array([a.elapsed_time(b) * 1e3 for a, b in ev])
     total_ms_max = max_over_ranks(total_ms)
     value = world * args.steps / (total_ms_max / 1e3)
-    bit_err_last = int(pipe.bit_err.sum().item())
+    bit_err_last = int(fs_dev.result(last_ticket[0])[1].sum().item())
+    del fs_dev
 
     # ---------------- latency distribution: graph replays on resident frames ----------------
     lat = []
@@ -443,35 +452,38 @@ def main():
                 "kernels": per_kernel}
 
     # ---------------- end to end through the public API (host buffers) ----------------
-    lab_h = torch.empty((1, K_USERS, N_DATA), dtype=torch.uint8).pin_memory()
-    cnt_h = torch.empty((2, 1, K_USERS), dtype=torch.int64).pin_memory()
+    # FrameStream: frame i's H2D (pinned) overlaps frame i-1's compute, its
+    # decisions + counters come back while frame i+1 computes; every copy of
+    # every step is inside the timed region
+    fs = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32", depth=2,
+                       post=post)
     h2d = rx_pin[0:1].numel() * 4 + pil_pin[0:1].numel() * 4 + tx_pin[0:1].numel()
-    d2h = lab_h.numel() + cnt_h.numel() * 8
+    d2h = fs.labels_h[0].numel() + fs.counts_h[0].numel() * 8
 
-    def e2e_step(i):
-        j = i % P
-        pipe.load(rx_pin[j:j + 1], pil_pin[j:j + 1], tx_pin[j:j + 1], non_blocking=True)
-        pipe.replay()
-        if world > 1:
-            D.gather_decisions(pipe.labels)
-            D.reduce_counts(pipe.bit_err)
-        lab_h.copy_(pipe.labels, non_blocking=True)
-        cnt_h[0].copy_(pipe.bit_err, non_blocking=True)
-        cnt_h[1].copy_(pipe.sym_err, non_blocking=True)
+    def e2e_run(n, i0, start=None):
+        t = None
+        for i in range(n):
+            j = (i0 + i) % P
+            t = fs.submit(rx_pin[j:j + 1], pil_pin[j:j + 1], tx_pin[j:j + 1],
+                          start_event=start if i == 0 else None)
+        cur = torch.cuda.current_stream()
+        for k in range(max(0, t - fs.depth + 1), t + 1):
+            cur.wait_event(fs.done_event(k))
+        return t
 
-    for i in range(args.warmup):
-        e2e_step(i)
+    e2e_run(args.warmup, 0)
     torch.cuda.synchronize()
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for i in range(args.steps):
-        e2e_step(i)
+    last = e2e_run(args.steps, args.warmup, start=a)
     b.record()
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(a.elapsed_time(b))
     e2e_value = world * args.steps / (e2e_ms / 1e3)
+    e2e_bit_err = int(fs.result(last)[1].sum().item())
+    del fs
 
     # ---------------- throughput mode: many frames per launch ----------------
     thr = None
@@ -535,7 +547,10 @@ def main():
               "roofline": roofline,
               "cpu_baseline": cpu,
               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                      "d2h_bytes_per_step": int(d2h)},
+                      "d2h_bytes_per_step": int(d2h),
+                      "api": "FrameStream (pinned host frames, H2D/D2H overlapped with the "
+                             "previous/next frame's compute, depth 2)",
+                      "bit_errors_last_step": e2e_bit_err},
               "throughput_mode": thr,
               "other_configs": others,
               "gpu_launches": launches_per_step * args.steps,

@@ -24,7 +24,7 @@ from . import _lib
 from .apsm import ApsmConfig, qtab_device
 from .noma import get_constellation, points_device
 
-__all__ = ["FramePipeline", "host_frames"]
+__all__ = ["FramePipeline", "FrameStream", "host_frames"]
 
 
 def _ld(n: int) -> int:
@@ -182,6 +182,89 @@ class FramePipeline:
             e = self.est.cpu().numpy().astype(np.float64)
             out["est"] = e[..., 0] + 1j * e[..., 1]
         return out
+
+
+class FrameStream:
+    """Streaming frames from pinned host memory with copy/compute overlap
+    (pinned, double-buffered H2D).
+
+    ``depth`` FramePipelines (each captured into its own CUDA graph) are used
+    round-robin.  Frame i's host->device copy runs on an H2D stream while frame
+    i-1 computes; its decisions and error counters come back on a D2H stream
+    while frame i+1 computes.  Every copy and launch is stream-ordered through
+    events, nothing blocks the host until ``result``::
+
+        fs = FrameStream(6, 16, 685, 3840)
+        t = fs.submit(rx_pin, pilots_pin, tx_pin)     # pinned host tensors, 1 frame
+        labels, bit_err, sym_err = fs.result(t)       # host tensors (pinned)
+    """
+
+    def __init__(self, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
+                 cfg: Optional[ApsmConfig] = None, precision: str = "f32", depth: int = 2,
+                 device=None, post=None):
+        if depth < 1:
+            raise ValueError(f"depth must be >= 1, got {depth}")
+        dev = dv.device() if device is None else device
+        self.depth = depth
+        self.pipes = [FramePipeline(1, K, M, n_train, n_data, scheme, cfg=cfg,
+                                    precision=precision, store_est=False, device=dev)
+                      for _ in range(depth)]
+        for p in self.pipes:
+            p.capture()
+        torch.cuda.synchronize(dev)
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        self.labels_h = [pin(p.labels) for p in self.pipes]
+        self.counts_h = [pin(torch.stack([p.bit_err, p.sym_err])) for p in self.pipes]
+        ev = lambda: [torch.cuda.Event() for _ in range(depth)]
+        self.ev_in, self.ev_comp, self.ev_out = ev(), ev(), ev()
+        self.used = [False] * depth
+        self.post = post          # optional callable(pipe) on the compute stream (collectives)
+        self.n = 0
+
+    def submit(self, rx, pilots, tx_labels, start_event=None) -> int:
+        """Queue one frame (pinned host tensors shaped like FramePipeline.load's
+        inputs for F = 1).  Returns a ticket for ``result``."""
+        i, slot = self.n, self.n % self.depth
+        p = self.pipes[slot]
+        comp = torch.cuda.current_stream(p.rx.device)
+        with torch.cuda.stream(self.h2d):
+            if start_event is not None:
+                self.h2d.wait_event(start_event)
+            if self.used[slot]:
+                self.h2d.wait_event(self.ev_comp[slot])     # the graph read this slot's inputs
+            p.load(rx, pilots, tx_labels, non_blocking=True)
+            self.ev_in[slot].record(self.h2d)
+        comp.wait_event(self.ev_in[slot])
+        if self.used[slot]:
+            comp.wait_event(self.ev_out[slot])              # outputs of the last use copied out
+        p.replay()
+        if self.post is not None:
+            self.post(p)
+        self.ev_comp[slot].record(comp)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.ev_comp[slot])
+            self.labels_h[slot].copy_(p.labels, non_blocking=True)
+            self.counts_h[slot][0].copy_(p.bit_err, non_blocking=True)
+            self.counts_h[slot][1].copy_(p.sym_err, non_blocking=True)
+            self.ev_out[slot].record(self.d2h)
+        self.used[slot] = True
+        self.n += 1
+        return i
+
+    def done_event(self, ticket: int):
+        """Event recorded after the ticket's results reached host memory."""
+        return self.ev_out[ticket % self.depth]
+
+    def result(self, ticket: int):
+        """(labels, bit_err, sym_err) of a submitted frame, as host tensors.
+        Valid until the slot is reused (``depth`` submissions later)."""
+        if ticket < self.n - self.depth or ticket >= self.n:
+            raise ValueError(f"ticket {ticket} is no longer (or not yet) held")
+        slot = ticket % self.depth
+        self.ev_out[slot].synchronize()
+        return self.labels_h[slot], self.counts_h[slot][0], self.counts_h[slot][1]
 
 
 def host_frames(seeds, K, M, n_train, n_data, scheme="QPSK", snr_db=20.0):

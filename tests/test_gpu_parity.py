@@ -367,3 +367,31 @@ def test_run_trial_reference_cases():
         K.run_trial(K.draw_channel(2, 2, "uniform", 0.0, np.random.default_rng(43)),
                     K.FrameSpec(10, 10), K.ApsmConfig(), K.EngineConfig(), 5,
                     np.random.default_rng(0))
+
+
+def test_frame_stream_matches_pipeline():
+    """FrameStream (overlapped pinned H2D/D2H) == one FramePipeline per frame."""
+    import torch
+    Kk, M, nt, nd = 3, 8, 120, 200
+    rx, pil, tx, _ = K.host_frames(range(5), Kk, M, nt, nd, "QPSK")
+    rx_p = torch.from_numpy(np.stack([rx.real, rx.imag], -1).astype(np.float32)).pin_memory()
+    pil_p = torch.from_numpy(np.stack([pil.real, pil.imag], -1).astype(np.float32)).pin_memory()
+    tx_p = torch.from_numpy(tx.astype(np.uint8)).pin_memory()
+    fs = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=2)
+    ref = K.FramePipeline(1, Kk, M, nt, nd, "QPSK", precision="f32")
+    got = []
+    for i in range(5):
+        t = fs.submit(rx_p[i:i + 1], pil_p[i:i + 1], tx_p[i:i + 1])
+        if i >= 1:
+            lab, be, se = fs.result(t - 1)
+            got.append((t - 1, lab.clone(), be.clone(), se.clone()))
+    lab, be, se = fs.result(4)
+    got.append((4, lab.clone(), be.clone(), se.clone()))
+    with pytest.raises(ValueError):
+        fs.result(0)
+    for i, lab, be, se in got:
+        ref.load(rx[i:i + 1], pil[i:i + 1], tx[i:i + 1])
+        ref.launch()
+        r = ref.results(est=False)
+        assert np.array_equal(lab.numpy(), r["labels"])
+        assert np.array_equal(be.numpy(), r["bit_err"]) and np.array_equal(se.numpy(), r["sym_err"])
