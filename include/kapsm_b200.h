@@ -52,6 +52,10 @@ typedef struct {
 const char* kapsm_strerror(int code);
 /* ABI version (major*100 + minor). */
 int kapsm_abi_version(void);
+/* A fresh non-blocking CUDA stream (host frameworks that pool their streams
+ * can hand out aliases; the overlapped pipeline needs two distinct ones). */
+int kapsm_stream_create(void** stream);
+int kapsm_stream_destroy(void* stream);
 /* Largest APSM window W supported by kapsm_train_* in this build. */
 int kapsm_max_window(void);
 /* Upper bound on realified training samples per (frame, user); the

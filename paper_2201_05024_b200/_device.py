@@ -23,6 +23,16 @@ def stream() -> C.c_void_p:
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def new_stream() -> torch.cuda.ExternalStream:
+    """A distinct CUDA stream created by the C library (torch.cuda.Stream() hands
+    out streams from a small round-robin pool, so two of them can alias).  It
+    lives as long as the process: torch's pinned-memory allocator may still
+    record events on it while tensors are freed at exit."""
+    h = C.c_void_p()
+    _lib.check(_lib.load().kapsm_stream_create(C.byref(h)), "stream_create")
+    return torch.cuda.ExternalStream(h.value, device=device())
+
+
 def ptr(t) -> C.c_void_p:
     if t is None:
         return C.c_void_p(None)

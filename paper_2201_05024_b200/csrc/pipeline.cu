@@ -135,3 +135,15 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
   }
 KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f32, float)
 KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f64, double)
+
+extern "C" int kapsm_stream_create(void** stream) {
+  if (!stream) return KAPSM_ERR_INVALID;
+  cudaStream_t t;
+  if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) != cudaSuccess) return KAPSM_ERR_CUDA;
+  *stream = t;
+  return KAPSM_OK;
+}
+
+extern "C" int kapsm_stream_destroy(void* stream) {
+  return cudaStreamDestroy((cudaStream_t)stream) == cudaSuccess ? KAPSM_OK : KAPSM_ERR_CUDA;
+}

@@ -81,7 +81,7 @@ class FramePipeline:
         if overlap:
             nbytes = int(lib.kapsm_screen_workspace_bytes(F, n_train, n_data))
             self.live = torch.zeros(((nbytes + 15) // 16 * 4,), dtype=torch.int32, device=dev)
-            self._side = torch.cuda.Stream(device=dev)
+            self._side = dv.new_stream()
             self._fn = dv.fn("kapsm_run_frames_overlap", precision)
         else:
             self.live = None
@@ -191,8 +191,10 @@ class FrameStream:
     ``depth`` FramePipelines (each captured into its own CUDA graph) are used
     round-robin.  Frame i's host->device copy runs on an H2D stream while frame
     i-1 computes; its decisions and error counters come back on a D2H stream
-    while frame i+1 computes.  Every copy and launch is stream-ordered through
-    events, nothing blocks the host until ``result``::
+    while frame i+1 computes.  With ``concurrent`` each slot computes on its own
+    stream, so up to ``depth`` frames are in flight at once (a frame's trainer
+    occupies a few SMs for most of its latency).  Every copy and launch is
+    stream-ordered through events, nothing blocks the host until ``result``::
 
         fs = FrameStream(6, 16, 685, 3840)
         t = fs.submit(rx_pin, pilots_pin, tx_pin)     # pinned host tensors, 1 frame
@@ -201,7 +203,7 @@ class FrameStream:
 
     def __init__(self, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32", depth: int = 2,
-                 device=None, post=None):
+                 device=None, post=None, concurrent: bool = False):
         if depth < 1:
             raise ValueError(f"depth must be >= 1, got {depth}")
         dev = dv.device() if device is None else device
@@ -212,8 +214,8 @@ class FrameStream:
         for p in self.pipes:
             p.capture()
         torch.cuda.synchronize(dev)
-        self.h2d = torch.cuda.Stream(device=dev)
-        self.d2h = torch.cuda.Stream(device=dev)
+        self.h2d = dv.new_stream()
+        self.d2h = dv.new_stream()
         pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         self.labels_h = [pin(p.labels) for p in self.pipes]
         self.counts_h = [pin(torch.stack([p.bit_err, p.sym_err])) for p in self.pipes]
@@ -221,14 +223,19 @@ class FrameStream:
         self.ev_in, self.ev_comp, self.ev_out = ev(), ev(), ev()
         self.used = [False] * depth
         self.post = post          # optional callable(pipe) on the compute stream (collectives)
+        self.comp = [dv.new_stream() for _ in range(depth)] if concurrent else None
+        self.ev_start = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
+        self.ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
         self.n = 0
 
-    def submit(self, rx, pilots, tx_labels, start_event=None) -> int:
+    def submit(self, rx, pilots, tx_labels, start_event=None, timing=None) -> int:
         """Queue one frame (pinned host tensors shaped like FramePipeline.load's
-        inputs for F = 1).  Returns a ticket for ``result``."""
+        inputs for F = 1).  ``start_event``: the H2D waits for it; ``timing``:
+        a (start, end) pair of timing events recorded around the frame's
+        compute.  Returns a ticket for ``result``."""
         i, slot = self.n, self.n % self.depth
         p = self.pipes[slot]
-        comp = torch.cuda.current_stream(p.rx.device)
+        comp = self.comp[slot] if self.comp else torch.cuda.current_stream(p.rx.device)
         with torch.cuda.stream(self.h2d):
             if start_event is not None:
                 self.h2d.wait_event(start_event)
@@ -239,9 +246,16 @@ class FrameStream:
         comp.wait_event(self.ev_in[slot])
         if self.used[slot]:
             comp.wait_event(self.ev_out[slot])              # outputs of the last use copied out
-        p.replay()
-        if self.post is not None:
-            self.post(p)
+        with torch.cuda.stream(comp):
+            self.ev_start[slot].record(comp)
+            if timing is not None:
+                timing[0].record(comp)
+            p.replay()
+            if self.post is not None:
+                self.post(p)
+            self.ev_end[slot].record(comp)
+            if timing is not None:
+                timing[1].record(comp)
         self.ev_comp[slot].record(comp)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.ev_comp[slot])
@@ -252,6 +266,12 @@ class FrameStream:
         self.used[slot] = True
         self.n += 1
         return i
+
+    def compute_us(self, ticket: int) -> float:
+        """Device time of the ticket's frame on its compute stream (after it completed)."""
+        slot = ticket % self.depth
+        self.ev_end[slot].synchronize()
+        return self.ev_start[slot].elapsed_time(self.ev_end[slot]) * 1e3
 
     def done_event(self, ticket: int):
         """Event recorded after the ticket's results reached host memory."""
