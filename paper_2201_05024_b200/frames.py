@@ -224,6 +224,7 @@ class FrameStream:
         self.used = [False] * depth
         self.post = post          # optional callable(pipe) on the compute stream (collectives)
         self.comp = [dv.new_stream() for _ in range(depth)] if concurrent else None
+        self.coll = dv.new_stream() if (concurrent and post is not None) else None
         self.ev_start = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
         self.ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
         self.n = 0
@@ -251,11 +252,18 @@ class FrameStream:
             if timing is not None:
                 timing[0].record(comp)
             p.replay()
-            if self.post is not None:
+            if self.post is not None and self.coll is None:
                 self.post(p)
             self.ev_end[slot].record(comp)
             if timing is not None:
                 timing[1].record(comp)
+        if self.coll is not None:
+            # collectives of all slots on ONE stream in submission order: every
+            # rank runs them in the same order whatever the slots' timing
+            self.coll.wait_event(self.ev_end[slot])
+            with torch.cuda.stream(self.coll):
+                self.post(p)
+            comp = self.coll
         self.ev_comp[slot].record(comp)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.ev_comp[slot])
