@@ -20,7 +20,8 @@ from .apsm import (ApsmConfig, ApsmTrainer, DegenerateSampleError, DictionaryCap
                    realify_batch, train, uniform_weights, window_indices)
 from .engine import STAGES, EngineConfig, batch_detect, batch_evaluate
 from .frames import FramePipeline, FrameStream, host_frames
-from .kernels import FilterState, KernelParams, evaluate, from_expansion, self_kernel, zero_filter
+from .kernels import (FilterState, KernelParams, evaluate, from_expansion, inner_product, norm_sq,
+                      self_kernel, zero_filter)
 from .noma import (SCHEMES, ChannelModel, Constellation, FrameSpec, TrialReport, ber,
                    demodulate_hard, draw_channel, get_constellation, modulate, noise_var_for_snr,
                    run_trial, seeded_frame, symbol_labels, synthesize_received)

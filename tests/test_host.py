@@ -170,3 +170,18 @@ def test_oracle_not_imported_by_product():
             if src.endswith(".py"):
                 text = open(src).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, re.M), mod
+
+
+def test_inner_product_error_rules():
+    """Zero weights / dimension mismatch raise like kernels.py:209-248 (host-side, no GPU)."""
+    import paper_2201_05024_b200 as K
+    p_lin = K.KernelParams(1.0, 0.0, 0.05)
+    f = K.FilterState(np.array([1.0, 2.0]), np.array([[0.1, 0.2]]), np.array([0.5]))
+    with pytest.raises(ValueError):
+        K.inner_product(f, f, p_lin)                    # Gaussian weight zero, Gaussian part
+    g = K.FilterState(np.array([1.0, 2.0]), np.empty((0, 2)), np.empty(0))
+    assert K.inner_product(g, g, p_lin) == 5.0
+    with pytest.raises(ValueError):
+        K.inner_product(K.zero_filter(4), K.zero_filter(6), p_lin)
+    with pytest.raises(ValueError):
+        K.inner_product(g, g, K.KernelParams(0.0, 1.0, 0.05))   # linear weight zero
