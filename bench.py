@@ -43,8 +43,8 @@ WORKLOAD = "paper scenario C1/C2: 6 users QPSK, 16 Rx, 685 pilots + 3840 data sy
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--pool", type=int, default=256, help="distinct frames per rank (> L2)")
     ap.add_argument("--lat-samples", type=int, default=1000)
@@ -308,6 +308,33 @@ def main():
             tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---------------- correctness gate (no timing without it) ----------------
+    # C1 frame seed 0 vs the reference's own outputs for users 0 and 1
+    # (tests/golden/c1_s0_users01.npz, written by the unmodified reference):
+    # soft estimates within 1e-4, bit-error counts and atom counts identical.
+    gate = None
+    if rank == 0:
+        gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden",
+                             "c1_s0_users01.npz")
+        g = np.load(gpath)
+        rxg, pilg, txg, _ = K.host_frames([0], K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME)
+        gp = K.FramePipeline(1, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32")
+        gp.load(rxg, pilg, txg)
+        gp.launch()
+        rr = gp.results()
+        worst, same = 0.0, True
+        for u in (0, 1):
+            ref = g[f"u{u}_est"]
+            worst = max(worst, float(np.max(np.abs(rr["est"][0, u] - ref)) / np.max(np.abs(ref))))
+            same &= int(rr["bit_err"][0, u]) == int(g[f"u{u}_bit_err"])
+            same &= int(rr["n_active"][0, u]) == int(g[f"u{u}_n_atoms"])
+        gate = {"frame": "C1 seed 0, users 0-1 vs reference outputs", "max_rel_soft": worst,
+                "counts_identical": bool(same), "pass": bool(same and worst <= 1e-4)}
+        del gp
+        if not gate["pass"]:
+            emit({"metric": METRIC, "error": "correctness gate failed", "gate": gate})
+            return 1
+
     # ---------------- frame pool (distinct seeds per rank, > L2) ----------------
     P = args.pool
     seeds = [rank * 1_000_000 + i for i in range(P)]
@@ -557,6 +584,7 @@ def main():
                       "bit_errors_last_step": e2e_bit_err},
               "throughput_mode": thr,
               "other_configs": others,
+              "correctness_gate": gate,
               "gpu_launches": launches_per_step * args.steps,
               "bit_errors_last_step": bit_err_last,
               "clocks": clk})
