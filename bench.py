@@ -43,8 +43,8 @@ WORKLOAD = "paper scenario C1/C2: 6 users QPSK, 16 Rx, 685 pilots + 3840 data sy
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--pool", type=int, default=256, help="distinct frames per rank (> L2)")
     ap.add_argument("--lat-samples", type=int, default=1000)
@@ -243,17 +243,17 @@ def run_reference(args):
         return 0
     kind, _ = _cpu_kind()
     cores = cpu_cores()
-    procs = max(1, min(cores, K_USERS))
-    # one step = one frame (all users in parallel); a single user per step when
-    # K is large so that the whole run stays within a few minutes
-    per_step_users = K_USERS if args.steps + args.warmup <= 60 else 1
+    # one step = as many whole frames as the host cores can train at once
+    # ((frame, user) tasks, one process each, every core busy)
+    fps_step = max(1, cores // K_USERS)
+    procs = fps_step * K_USERS
     import multiprocessing as mp
     ctx = mp.get_context("fork")
     times = []
     errs = 0
     with ctx.Pool(procs) as pool:
         for i in range(args.warmup + args.steps):
-            tasks = [(100000 + i, u) for u in range(per_step_users)]
+            tasks = [(100000 + fps_step * i + k, u) for k in range(fps_step) for u in range(K_USERS)]
             t0 = time.perf_counter()
             res = pool.map(_cpu_task, tasks, chunksize=1)
             dt = time.perf_counter() - t0
@@ -262,20 +262,21 @@ def run_reference(args):
                 errs += sum(r[1] for r in res)
     import numpy as np
     tot = float(np.sum(times))
-    frames = len(times) * per_step_users / K_USERS
+    frames = len(times) * fps_step
     value = frames / tot
-    lat = np.array(times) * (K_USERS / per_step_users) * 1e6
+    lat = np.array(times) * 1e6
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
           "data": "synthetic (seeded, reference RNG order)",
-          "config": {"workload": WORKLOAD, "users_per_step": per_step_users,
+          "config": {"workload": WORKLOAD, "frames_per_step": fps_step,
                      "engine": "balanced, tile_inputs=256, workers=1 per process"},
           "latency_us": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
                          "n": int(lat.size), "note": "per-frame wall time, users in parallel"},
           "bit_errors": int(errs),
           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind,
-                           "sample": f"{per_step_users} user(s) x {len(times)} steps, one process per user"},
+                           "sample": (f"{fps_step} frame(s) x {K_USERS} users per step x "
+                                      f"{len(times)} steps, one process per (frame, user)")},
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     return 0
 
