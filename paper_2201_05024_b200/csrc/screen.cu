@@ -228,6 +228,10 @@ __global__ void __launch_bounds__(128)
                          unsigned long long* __restrict__ bit_err,
                          unsigned long long* __restrict__ sym_err) {
   __shared__ T pts[128];
+  // the CTA's 32 payload rows, staged with coalesced loads (one contiguous
+  // block of rx); odd row stride in (re, im) pairs: conflict-free pair reads
+  constexpr int YS = 2 * MT + 2;
+  __shared__ __align__(16) T ys[32 * YS];
   const int f = blockIdx.z;
   const int lane = threadIdx.x;
   const int u = blockIdx.y * blockDim.y + threadIdx.y;
@@ -235,13 +239,19 @@ __global__ void __launch_bounds__(128)
   const bool tvalid = t < n_data;
   const int NW = (n_train + 31) / 32, Np = 2 * n_train;
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int i = tid; i < 2 * n_points; i += blockDim.x * blockDim.y) pts[i] = points[i];
+  const int nthr = blockDim.x * blockDim.y;
+  for (int i = tid; i < 2 * n_points; i += nthr) pts[i] = points[i];
+  const T* Xf = rx + (long long)f * rx_stride;
+  {
+    const int t0 = blockIdx.x * 32, rows = min(32, n_data - t0), rl = 2 * M;
+    const T* src = Xf + (long long)(n_train + t0) * rl;
+    for (int e = tid; e < rows * rl; e += nthr) ys[(e / rl) * YS + e % rl] = src[e];
+  }
   __syncthreads();
   if (u >= K) return;
-  const T* Xf = rx + (long long)f * rx_stride;
   T y[2 * MT];
   {
-    const T* yp = Xf + (long long)(n_train + (tvalid ? t : 0)) * 2 * M;
+    const T* yp = ys + lane * YS;
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
       const bool in = tvalid && k < M;
