@@ -915,8 +915,51 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       const T* t0 = theta0 ? theta0 + (long long)fu * dim : nullptr;
       constexpr int nw = NG == 1 ? R::WARPS : NB + 1;
       const int ew = NG == 1 ? warp : role;
-      if (rx) {
-        // complex pilots: Theta = theta[:M] + i theta[M:] = w_l sum_p (c_2p - i c_2p+1) x_p
+      // the chain's tagged coefficient words are dead now: they hold the
+      // cross-warp partial sums of the coalesced form below
+      T* red = reinterpret_cast<T*>(ctag);
+      const bool coalesced = dim <= 128 && (size_t)nw * dim * sizeof(T) <= (size_t)(Np + TC_S) * SS;
+      if (rx && coalesced) {
+        // complex pilots: Theta = theta[:M] + i theta[M:] = w_l sum_p (c_2p - i c_2p+1) x_p.
+        // Lanes run over a pilot row's 2M interleaved components (coalesced
+        // rows), warps over pilots; pairs of lanes and then the warps (fixed
+        // order) are summed.
+        const int M = dim / 2, n_train = Np / 2;
+        const T* X = rx + (long long)f * rx_stride;
+        T A[4] = {T(0), T(0), T(0), T(0)}, Bq[4] = {T(0), T(0), T(0), T(0)};
+        const bool odd = lane & 1;
+#pragma unroll 4
+        for (int p = ew; p < n_train; p += nw) {
+          const T c1 = cfin[2 * p], c2 = cfin[2 * p + 1];
+          const T ca = odd ? c2 : c1, cb = odd ? c1 : -c2;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = lane + 32 * q;
+            if (e < dim) {
+              const T v = X[(long long)p * dim + e];
+              A[q] = fma(ca, v, A[q]);
+              Bq[q] = fma(cb, v, Bq[q]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const T a1 = __shfl_down_sync(0xffffffffu, A[q], 1);
+          const T b1 = __shfl_down_sync(0xffffffffu, Bq[q], 1);
+          const int e = lane + 32 * q;
+          if (!odd && e < dim) {
+            red[ew * dim + e / 2] = A[q] + a1;           // real part of component e/2
+            red[ew * dim + M + e / 2] = Bq[q] + b1;      // imaginary part
+          }
+        }
+        named_bar(group_bar, GT);
+        for (int e = gt; e < dim; e += GT) {
+          T acc = T(0);
+          for (int w = 0; w < nw; ++w) acc += red[w * dim + e];
+          th[e] = w_l * acc + (t0 ? t0[e] : T(0));
+        }
+      } else if (rx) {
+        // complex pilots, strided form (reduction buffer too small)
         const int M = dim / 2, n_train = Np / 2;
         const T* X = rx + (long long)f * rx_stride;
         for (int kk = ew; kk < M; kk += nw) {
@@ -938,6 +981,7 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
         const T* S = samples + (long long)f * samples_stride;
         for (int kk = ew; kk < dim; kk += nw) {
           T acc = T(0);
+#pragma unroll 8
           for (int i = lane; i < Np; i += 32) acc = fma(cfin[i], S[(long long)i * dim + kk], acc);
           acc = warp_sum(acc);
           if (lane == 0) th[kk] = w_l * acc + (t0 ? t0[kk] : T(0));

@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(TW_MAX_THREADS, 1)
         const T* X = rx + (long long)f * rx_stride;
         for (int kk = warp; kk < M; kk += nw) {
           T tr = T(0), ti = T(0);
+          // unrolled: 8 pilots' strided loads in flight per lane (same sum order)
+#pragma unroll 8
           for (int p = lane; p < n_train; p += 32) {
             const T c1 = cfin[2 * p], c2 = cfin[2 * p + 1];
             const T xr = X[(long long)p * 2 * M + 2 * kk], xi = X[(long long)p * 2 * M + 2 * kk + 1];
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(TW_MAX_THREADS, 1)
         const T* Sm = samples + (long long)f * samples_stride;
         for (int kk = warp; kk < dim; kk += nw) {
           T acc = T(0);
+#pragma unroll 8
           for (int i = lane; i < Np; i += 32) acc = fma(cfin[i], Sm[(long long)i * dim + kk], acc);
           acc = warp_sum(acc);
           if (lane == 0) th[kk] = w_l * acc + (t0 ? t0[kk] : T(0));
