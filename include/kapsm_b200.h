@@ -56,6 +56,20 @@ int kapsm_abi_version(void);
  * can hand out aliases; the overlapped pipeline needs two distinct ones). */
 int kapsm_stream_create(void** stream);
 int kapsm_stream_destroy(void* stream);
+/* Streaming frames (FrameStream): enqueue one frame's input copies
+ * (cudaMemcpyDefault: pinned host or device sources) on `h2d`, then its
+ * captured pipeline graph on `comp`; optional events: ev_wait0 (first copy
+ * waits), ev_inputs_free (the slot's previous graph read its inputs),
+ * ev_outputs_free (the slot's previous results were copied out), ev_t0/ev_t1
+ * (timing around the graph).  ev_in / ev_comp are recorded.  kapsm_stream_
+ * frame_out enqueues the result copies on `d2h` after ev_ready and records
+ * ev_out. */
+int kapsm_stream_frame_in(void* h2d, void* comp, void* ev_wait0, void* ev_inputs_free,
+                          void* ev_outputs_free, void* ev_in, int n, void* const* dst,
+                          const void* const* src, const unsigned long long* bytes,
+                          void* graph_exec, void* ev_t0, void* ev_t1, void* ev_comp);
+int kapsm_stream_frame_out(void* d2h, void* ev_ready, int n, void* const* dst,
+                           const void* const* src, const unsigned long long* bytes, void* ev_out);
 /* Largest APSM window W supported by kapsm_train_* in this build. */
 int kapsm_max_window(void);
 /* Upper bound on realified training samples per (frame, user); the

@@ -147,3 +147,45 @@ extern "C" int kapsm_stream_create(void** stream) {
 extern "C" int kapsm_stream_destroy(void* stream) {
   return cudaStreamDestroy((cudaStream_t)stream) == cudaSuccess ? KAPSM_OK : KAPSM_ERR_CUDA;
 }
+
+// Streaming frames: one call enqueues a frame's input copies (cudaMemcpyDefault:
+// pinned host or device sources) on the copy stream and its captured pipeline
+// graph on the slot's compute stream, ordered through the caller's events; a
+// second call enqueues the result copies.  The host cost per frame is one
+// library call each way instead of a dozen framework calls.
+extern "C" int kapsm_stream_frame_in(void* h2d, void* comp, void* ev_wait0, void* ev_inputs_free,
+                                     void* ev_outputs_free, void* ev_in, int n, void* const* dst,
+                                     const void* const* src, const unsigned long long* bytes,
+                                     void* graph_exec, void* ev_t0, void* ev_t1, void* ev_comp) {
+  cudaStream_t hs = (cudaStream_t)h2d, cs = (cudaStream_t)comp;
+  if (!ev_in || !ev_comp || !graph_exec || n < 0 || (n && (!dst || !src || !bytes)))
+    return KAPSM_ERR_INVALID;
+  if (ev_wait0 && cudaStreamWaitEvent(hs, (cudaEvent_t)ev_wait0, 0) != cudaSuccess) return KAPSM_ERR_CUDA;
+  if (ev_inputs_free && cudaStreamWaitEvent(hs, (cudaEvent_t)ev_inputs_free, 0) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  for (int i = 0; i < n; ++i)
+    if (cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDefault, hs) != cudaSuccess)
+      return KAPSM_ERR_CUDA;
+  if (cudaEventRecord((cudaEvent_t)ev_in, hs) != cudaSuccess ||
+      cudaStreamWaitEvent(cs, (cudaEvent_t)ev_in, 0) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  if (ev_outputs_free && cudaStreamWaitEvent(cs, (cudaEvent_t)ev_outputs_free, 0) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  if (ev_t0 && cudaEventRecord((cudaEvent_t)ev_t0, cs) != cudaSuccess) return KAPSM_ERR_CUDA;
+  if (cudaGraphLaunch((cudaGraphExec_t)graph_exec, cs) != cudaSuccess) return KAPSM_ERR_CUDA;
+  if (ev_t1 && cudaEventRecord((cudaEvent_t)ev_t1, cs) != cudaSuccess) return KAPSM_ERR_CUDA;
+  return cudaEventRecord((cudaEvent_t)ev_comp, cs) == cudaSuccess ? KAPSM_OK : KAPSM_ERR_CUDA;
+}
+
+extern "C" int kapsm_stream_frame_out(void* d2h, void* ev_ready, int n, void* const* dst,
+                                      const void* const* src, const unsigned long long* bytes,
+                                      void* ev_out) {
+  cudaStream_t ds = (cudaStream_t)d2h;
+  if (!ev_ready || !ev_out || n < 0 || (n && (!dst || !src || !bytes)))
+    return KAPSM_ERR_INVALID;
+  if (cudaStreamWaitEvent(ds, (cudaEvent_t)ev_ready, 0) != cudaSuccess) return KAPSM_ERR_CUDA;
+  for (int i = 0; i < n; ++i)
+    if (cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDefault, ds) != cudaSuccess)
+      return KAPSM_ERR_CUDA;
+  return cudaEventRecord((cudaEvent_t)ev_out, ds) == cudaSuccess ? KAPSM_OK : KAPSM_ERR_CUDA;
+}

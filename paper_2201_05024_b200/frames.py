@@ -105,9 +105,12 @@ class FramePipeline:
         put(self.tx, tx_labels, False)
 
     # -- compute ------------------------------------------------------------
-    def _args(self):
+    def _args(self, rx=None, pilots=None, tx=None):
         c = self.cfg
-        head = (dv.ptr(self.rx), self.T * self.M * 2, dv.ptr(self.pilots), dv.ptr(self.tx),
+        rx = self.rx if rx is None else rx
+        pilots = self.pilots if pilots is None else pilots
+        tx = self.tx if tx is None else tx
+        head = (dv.ptr(rx), self.T * self.M * 2, dv.ptr(pilots), dv.ptr(tx),
                 self.F, self.K, self.n_train, self.n_data, self.M, c.window, float(c.epsilon),
                 _lib.params(c.params), dv.ptr(self.qtab), dv.ptr(self.points), self.n_points,
                 self.bps, dv.ptr(self.gram), self.ld)
@@ -117,6 +120,24 @@ class FramePipeline:
         if self.overlap:
             return head + (dv.ptr(self.live),) + tail
         return head + tail
+
+    def launch_on(self, rx, pilots, tx_labels):
+        """Run the pipeline on device-resident inputs in place (no copy into
+        the static buffers): tensors shaped and typed like ``rx``/``pilots``/
+        ``tx`` (contiguous, same device).  Outputs land in this pipeline's
+        buffers.  Stream-ordered on the current stream; not graph-captured."""
+        for name, t, ref in (("rx", rx, self.rx), ("pilots", pilots, self.pilots),
+                             ("tx_labels", tx_labels, self.tx)):
+            if (not isinstance(t, torch.Tensor) or t.shape != ref.shape or t.dtype != ref.dtype
+                    or t.device != ref.device or not t.is_contiguous()):
+                raise ValueError(f"{name}: expected a contiguous {ref.dtype} tensor of shape "
+                                 f"{tuple(ref.shape)} on {ref.device}")
+        args = self._args(rx, pilots, tx_labels)
+        if self.overlap:
+            _lib.check(self._fn(*args, dv.stream(), C.c_void_p(self._side.cuda_stream)),
+                       "run_frames_overlap")
+        else:
+            _lib.check(self._fn(*args, dv.stream()), "run_frames")
 
     def launch(self, time_detect: bool = False):
         """Enqueue the whole pipeline on the current stream.  With time_detect,
@@ -184,6 +205,15 @@ class FramePipeline:
         return out
 
 
+def _event_handle(ev) -> int:
+    """Raw cudaEvent_t of a torch event (created by a first record if needed)."""
+    h = ev.cuda_event
+    if not h:
+        ev.record(torch.cuda.current_stream())
+        h = ev.cuda_event
+    return h
+
+
 class FrameStream:
     """Streaming frames from pinned host memory with copy/compute overlap
     (pinned, double-buffered H2D).
@@ -227,50 +257,69 @@ class FrameStream:
         self.coll = dv.new_stream() if (concurrent and post is not None) else None
         self.ev_start = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
         self.ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
+        lib = _lib.load()
+        self._fin, self._fout = lib.kapsm_stream_frame_in, lib.kapsm_stream_frame_out
+        VP, UL = C.c_void_p * 3, C.c_ulonglong * 3
+        self._slot = []
+        for k, p in enumerate(self.pipes):
+            # with no collectives the slot's "inputs free" point is the graph's end
+            comp_ev = self.ev_comp[k] if post is not None else self.ev_end[k]
+            self._slot.append({
+                "dst_in": VP(p.rx.data_ptr(), p.pilots.data_ptr(), p.tx.data_ptr()),
+                "bytes_in": UL(*(t.numel() * t.element_size() for t in (p.rx, p.pilots, p.tx))),
+                "src_in": VP(0, 0, 0),
+                "dst_out": VP(self.labels_h[k].data_ptr(), self.counts_h[k][0].data_ptr(),
+                              self.counts_h[k][1].data_ptr()),
+                "src_out": VP(p.labels.data_ptr(), p.bit_err.data_ptr(), p.sym_err.data_ptr()),
+                "bytes_out": UL(p.labels.numel(), p.bit_err.numel() * 8, p.sym_err.numel() * 8),
+                "graph": p.graph.raw_cuda_graph_exec(),
+                "ev_in": _event_handle(self.ev_in[k]), "ev_comp": _event_handle(comp_ev),
+                "ev_out": _event_handle(self.ev_out[k]), "ev_end": _event_handle(self.ev_end[k]),
+                "ev_start": _event_handle(self.ev_start[k]),
+            })
         self.n = 0
 
     def submit(self, rx, pilots, tx_labels, start_event=None, timing=None) -> int:
-        """Queue one frame (pinned host tensors shaped like FramePipeline.load's
-        inputs for F = 1).  ``start_event``: the H2D waits for it; ``timing``:
-        a (start, end) pair of timing events recorded around the frame's
-        compute.  Returns a ticket for ``result``."""
+        """Queue one frame: tensors shaped like FramePipeline.load's inputs for
+        F = 1 (float32/float64 interleaved rx and pilots, uint8 labels), pinned
+        host or device-resident; they are copied into the slot's buffers on the
+        copy stream and the slot's captured graph runs on its compute stream --
+        one library call (``kapsm_stream_frame_in``), results come back with a
+        second (``kapsm_stream_frame_out``).  ``start_event``: the first copy
+        waits for it; ``timing``: a (start, end) pair of timing events recorded
+        around the frame's compute.  Returns a ticket for ``result``."""
         i, slot = self.n, self.n % self.depth
         p = self.pipes[slot]
+        sl = self._slot[slot]
+        for t, ref in ((rx, p.rx), (pilots, p.pilots), (tx_labels, p.tx)):
+            if t.dtype != ref.dtype or t.numel() != ref.numel() or not t.is_contiguous():
+                raise ValueError(f"frame tensor {tuple(t.shape)} {t.dtype} does not match "
+                                 f"{tuple(ref.shape)} {ref.dtype}")
+        src = sl["src_in"]
+        src[0], src[1], src[2] = rx.data_ptr(), pilots.data_ptr(), tx_labels.data_ptr()
+        used = self.used[slot]
+        t0, t1 = sl["ev_start"], None
+        if timing is not None:
+            t0, t1 = _event_handle(timing[0]), _event_handle(timing[1])
         comp = self.comp[slot] if self.comp else torch.cuda.current_stream(p.rx.device)
-        with torch.cuda.stream(self.h2d):
-            if start_event is not None:
-                self.h2d.wait_event(start_event)
-            if self.used[slot]:
-                self.h2d.wait_event(self.ev_comp[slot])     # the graph read this slot's inputs
-            p.load(rx, pilots, tx_labels, non_blocking=True)
-            self.ev_in[slot].record(self.h2d)
-        comp.wait_event(self.ev_in[slot])
-        if self.used[slot]:
-            comp.wait_event(self.ev_out[slot])              # outputs of the last use copied out
-        with torch.cuda.stream(comp):
-            self.ev_start[slot].record(comp)
-            if timing is not None:
-                timing[0].record(comp)
-            p.replay()
-            if self.post is not None and self.coll is None:
+        _lib.check(self._fin(
+            self.h2d.cuda_stream, comp.cuda_stream,
+            _event_handle(start_event) if start_event is not None else None,
+            sl["ev_comp"] if used else None, sl["ev_out"] if used else None, sl["ev_in"],
+            3, sl["dst_in"], src, sl["bytes_in"], sl["graph"], t0, t1, sl["ev_end"]),
+            "stream_frame_in")
+        ready = sl["ev_end"]
+        if self.post is not None:
+            coll = self.coll if self.coll is not None else comp
+            coll.wait_event(self.ev_end[slot])
+            with torch.cuda.stream(coll):
                 self.post(p)
-            self.ev_end[slot].record(comp)
-            if timing is not None:
-                timing[1].record(comp)
-        if self.coll is not None:
-            # collectives of all slots on ONE stream in submission order: every
-            # rank runs them in the same order whatever the slots' timing
-            self.coll.wait_event(self.ev_end[slot])
-            with torch.cuda.stream(self.coll):
-                self.post(p)
-            comp = self.coll
-        self.ev_comp[slot].record(comp)
-        with torch.cuda.stream(self.d2h):
-            self.d2h.wait_event(self.ev_comp[slot])
-            self.labels_h[slot].copy_(p.labels, non_blocking=True)
-            self.counts_h[slot][0].copy_(p.bit_err, non_blocking=True)
-            self.counts_h[slot][1].copy_(p.sym_err, non_blocking=True)
-            self.ev_out[slot].record(self.d2h)
+            self.ev_comp[slot].record(coll)
+            ready = sl["ev_comp"]
+        else:
+            ready = sl["ev_end"]
+        _lib.check(self._fout(self.d2h.cuda_stream, ready, 3, sl["dst_out"], sl["src_out"],
+                              sl["bytes_out"], sl["ev_out"]), "stream_frame_out")
         self.used[slot] = True
         self.n += 1
         return i

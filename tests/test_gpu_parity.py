@@ -389,6 +389,21 @@ def test_frame_stream_matches_pipeline():
     got.append((4, lab.clone(), be.clone(), se.clone()))
     with pytest.raises(ValueError):
         fs.result(0)
+    # device-resident frames: read in place by direct launches, concurrent slots
+    fd = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=3, concurrent=True)
+    rx_d, pil_d, tx_d = rx_p.cuda(), pil_p.cuda(), tx_p.cuda()
+    dev_got = {}
+    for i in range(5):
+        t = fd.submit(rx_d[i:i + 1], pil_d[i:i + 1], tx_d[i:i + 1])
+        if i >= 2:
+            lab, be, _ = fd.result(t - 2)
+            dev_got[t - 2] = (lab.clone(), be.clone())
+    for t in (3, 4):
+        lab, be, _ = fd.result(t)
+        dev_got[t] = (lab.clone(), be.clone())
+    for i, lab, be, se in got:
+        assert np.array_equal(dev_got[i][0].numpy(), lab.numpy())
+        assert np.array_equal(dev_got[i][1].numpy(), be.numpy())
     for i, lab, be, se in got:
         ref.load(rx[i:i + 1], pil[i:i + 1], tx[i:i + 1])
         ref.launch()
