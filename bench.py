@@ -366,7 +366,8 @@ def main():
     # device-resident steps: the pool frame is copied into one of two captured
     # pipelines on a copy stream while the previous frame computes (FrameStream)
     fs_dev = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32",
-                           depth=args.inflight, concurrent=args.inflight > 1, post=post)
+                           depth=args.inflight, concurrent=args.inflight > 1,
+                           post=post if world > 1 else None)
     last_ticket = [0]
 
     def step(i, start=None, timing=None):
@@ -383,12 +384,14 @@ def main():
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    from paper_2201_05024_b200.frames import _event_handle
+    evh = [(_event_handle(a), _event_handle(b)) for a, b in ev]   # raw handles: cheap submits
     e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
     e_all0.record()
     for i in range(args.steps):
-        step(args.warmup + i, start=e_all0 if i == 0 else None, timing=ev[i])
+        step(args.warmup + i, start=e_all0 if i == 0 else None, timing=evh[i])
     cur = torch.cuda.current_stream()
     for k in range(max(0, last_ticket[0] - fs_dev.depth + 1), last_ticket[0] + 1):
         cur.wait_event(fs_dev.done_event(k))
@@ -485,7 +488,8 @@ def main():
     # decisions + counters come back while frame i+1 computes; every copy of
     # every step is inside the timed region
     fs = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32",
-                       depth=args.inflight, concurrent=args.inflight > 1, post=post)
+                       depth=args.inflight, concurrent=args.inflight > 1,
+                       post=post if world > 1 else None)
     h2d = rx_pin[0:1].numel() * 4 + pil_pin[0:1].numel() * 4 + tx_pin[0:1].numel()
     d2h = fs.labels_h[0].numel() + fs.counts_h[0].numel() * 8
 

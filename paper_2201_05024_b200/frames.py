@@ -299,8 +299,8 @@ class FrameStream:
         src[0], src[1], src[2] = rx.data_ptr(), pilots.data_ptr(), tx_labels.data_ptr()
         used = self.used[slot]
         t0, t1 = sl["ev_start"], None
-        if timing is not None:
-            t0, t1 = _event_handle(timing[0]), _event_handle(timing[1])
+        if timing is not None:          # torch events or their raw handles
+            t0, t1 = (h if isinstance(h, int) else _event_handle(h) for h in timing)
         comp = self.comp[slot] if self.comp else torch.cuda.current_stream(p.rx.device)
         _lib.check(self._fin(
             self.h2d.cuda_stream, comp.cuda_stream,
