@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--throughput-frames", type=int, default=296)
     ap.add_argument("--cpu-frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--inflight", type=int, default=4,
+    ap.add_argument("--inflight", type=int, default=6,
                     help="frames in flight (FrameStream depth, one compute stream each)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the single-frame latency of the other BASELINE configs (C3/C4)")

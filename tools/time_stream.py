@@ -11,7 +11,7 @@ tx_p = torch.from_numpy(tx.astype(np.uint8)).pin_memory()
 src = {"host": (rx_p, pil_p, tx_p), "device": (rx_p.cuda(), pil_p.cuda(), tx_p.cuda())}
 for where in ("device", "host"):
     r, p_, t_ = src[where]
-    for depth, conc in ((2, False), (2, True), (3, True), (4, True), (6, True)):
+    for depth, conc in ((4, True), (6, True), (8, True), (12, True)):
         fs = K.FrameStream(6, 16, 685, 3840, depth=depth, concurrent=conc)
         for i in range(8):
             last = fs.submit(r[i % P:i % P + 1], p_[i % P:i % P + 1], t_[i % P:i % P + 1])
