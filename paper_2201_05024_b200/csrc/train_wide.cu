@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(TW_MAX_THREADS, 1)
       const unsigned kcol = kb_s + (unsigned)i * TS;                 // Kb[.][i]
       const unsigned krow = kb_s + (unsigned)(i * S) * TS;           // Kb[i][.]
       const unsigned rowstep = (unsigned)S * TS;
+      const T qmW = lds_t<T>(qsm_s + (unsigned)(2 * (W - 1)) * TS);
+      const T qlW = lds_t<T>(qsm_s + (unsigned)(2 * (W - 1) + 1) * TS);
       int mq = (P + Q) % S;                       // ring position of sample n+P+Q
       int dq = ((P + Q - i) % S + S) % S;         // (n+P+Q - i) mod S
       int jlo = 0;                                // ring position of lo_n
@@ -197,6 +199,11 @@ __global__ void __launch_bounds__(TW_MAX_THREADS, 1)
         }
         const int lo = n - W + 1 > 0 ? n - W + 1 : 0;
         bool stalled = false;
+        if (valid && s == n + 1) {                // one step ahead: 1/kappa(r_s, r_s) off the entry step
+          const T den = lds_t<T>(krow + (unsigned)i * TS);   // band row of s landed at step s-P
+          if (!(den > T(0))) degen = 1;
+          invden = den > T(0) ? T(1) / den : T(0);
+        }
         if (valid && s == n) {                    // entering: init_m from the helpers
           T iv = T(0);
           long long spins = 0;
@@ -205,16 +212,20 @@ __global__ void __launch_bounds__(TW_MAX_THREADS, 1)
               stalled = true;
               break;
             }
-          const T den = lds_t<T>(krow + (unsigned)i * TS);
-          if (!(den > T(0))) degen = 1;
-          invden = den > T(0) ? T(1) / den : T(0);
+          if (s == 0) {                           // (no step before sample 0)
+            const T den = lds_t<T>(krow + (unsigned)i * TS);
+            if (!(den > T(0))) degen = 1;
+            invden = den > T(0) ? T(1) / den : T(0);
+          }
           bm = bv - eps - iv;
           bp = bv + eps - iv;
         }
         T delta = T(0);
         if (valid && s >= lo && s <= n) {
           const int J = n - lo + 1;
-          const T q = lds_t<T>(qsm_s + (unsigned)(2 * (J - 1) + (s == n)) * TS);
+          // full windows (J = W) after warm-up: the two weights live in registers
+          const T q = J == W ? (s == n ? qlW : qmW)
+                             : lds_t<T>(qsm_s + (unsigned)(2 * (J - 1) + (s == n)) * TS);
           const T qi = q * invden;
           const T v1 = fma(-qi, Y, qi * bm), v2 = fma(-qi, Y, qi * bp);
           delta = fmax(v1, T(0)) + fmin(v2, T(0));
