@@ -57,7 +57,7 @@ constexpr int TC_SRING = 4;                 // staged column batches (ring, pow2
 constexpr int TC_INIT = 64;                 // init values (ring, pow2)
 constexpr int TC_ERING = 128;               // early init parts in flight (tagged ring, pow2)
 constexpr int TC_Q = 61;                    // init: early part i <= m - Q, late part <= 32 elements
-constexpr int TC_MAX_NP = 3072;
+constexpr int TC_MAX_NP = 16384;            // (and the shared-memory footprint)
 // slot reuse: the batch taken over after step n+1 (samples n+D..n+D+3)
 // reuses the slots of samples that left the window by step n+1:
 // D + 3 + W - 33 <= 1.
@@ -359,8 +359,10 @@ template <> struct Roles<4, 1> {
 template <typename T, int NG, int CL>
 struct GroupSmem {
   // byte offsets of one group's region in dynamic shared memory
-  size_t dv, snap, stage, initr, ering, ctag, cfin, fsfin, bsm, qsm, ctl, total;
-  __host__ __device__ GroupSmem(int W, int Np) {
+  size_t dv, snap, stage, tst, bsm, initr, ering, ctag, cfin, fsfin, qsm, ctl, total;
+  // staged: the batch targets arrive with the staged columns instead of a
+  // per-sample array (larger Np fits in shared memory)
+  __host__ __device__ GroupSmem(int W, int Np, bool staged = false) {
     using Slot = typename Tagged<T>::slot_t;
     constexpr int NB = Roles<NG, CL>::NB;
     size_t o = 0;
@@ -368,12 +370,13 @@ struct GroupSmem {
     dv = take(2 * TC_S * sizeof(T));
     snap = take((size_t)2 * TC_S * sizeof(T));   // slot coefficients after a block's 1st step
     stage = take((size_t)TC_SRING * TC_BT * TC_S * sizeof(T));
+    tst = take((size_t)TC_SRING * TC_BT * sizeof(T));   // the staged batches' targets
+    bsm = take(staged ? 0 : (size_t)(Np + 2 * TC_S) * sizeof(T));   // all targets (zero padded)
     initr = take((size_t)TC_INIT * sizeof(Slot));
     ering = take((size_t)TC_ERING * sizeof(Slot));
     ctag = take((size_t)(Np + TC_S) * sizeof(Slot));
     cfin = take((size_t)(Np + TC_S) * sizeof(T));
     fsfin = take((size_t)(Np + TC_S) * sizeof(int));
-    bsm = take((size_t)(Np + 2 * TC_S) * sizeof(T));
     qsm = take(2 * (size_t)(W + 1) * sizeof(T));
     ctl = take(16 * sizeof(int));
     total = (o + 127) & ~size_t(127);
@@ -398,7 +401,7 @@ __device__ __noinline__ void init_spin(unsigned a, bool isent, int me, int Np, T
   }
 }
 
-template <typename T, int NG, int CL, int WM, bool DBG>
+template <typename T, int NG, int CL, int WM, bool DBG, bool STG = false>
 __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
     apsm_train_kernel(const T* __restrict__ gram, long long ld, long long gram_stride,
                       const T* __restrict__ rx, long long rx_stride,
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
   constexpr int FIRST = D;                    // first sample whose init needs coefficients
   constexpr unsigned TS = sizeof(T), SS = sizeof(Slot);
   extern __shared__ __align__(128) unsigned char smem[];
-  const GroupSmem<T, NG, CL> L(W, Np);
+  const GroupSmem<T, NG, CL> L(W, Np, STG);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned rank = CL > 1 ? cluster_rank() : 0u;
   const int grp = R::group(warp);
@@ -435,7 +438,6 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
   Slot* ctag = reinterpret_cast<Slot*>(gs + L.ctag);     // [Np+S] tagged final c_m
   T* cfin = reinterpret_cast<T*>(gs + L.cfin);           // [Np+S] final c_m (stored before ctag)
   int* fsfin = reinterpret_cast<int*>(gs + L.fsfin);     // [Np+S] first-activation step
-  T* bsm = reinterpret_cast<T*>(gs + L.bsm);             // [Np+2S] targets (zero padded)
   T* qsm = reinterpret_cast<T*>(gs + L.qsm);             // [W+1][2] (q_mid, q_last), row W = 0
   int* ctl = reinterpret_cast<int*>(gs + L.ctl);         // [1]=abort [2]=status [3]=nact
   const int group_bar = 1 + grp;
@@ -467,7 +469,10 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       for (int i = gt; i < TC_ERING; i += GT) Tagged<T>::store(&ering[i], T(0), -1);
     }
     for (int i = gt; i < Np + TC_S; i += GT) { Tagged<T>::store(&ctag[i], T(0), -1); fsfin[i] = -1; }
-    for (int i = gt; i < Np + 2 * TC_S; i += GT) bsm[i] = i < Np ? B[i] : T(0);
+    if (!STG) {
+      T* bsm = reinterpret_cast<T*>(gs + L.bsm);         // [Np+2S] targets (zero padded)
+      for (int i = gt; i < Np + 2 * TC_S; i += GT) bsm[i] = i < Np ? B[i] : T(0);
+    }
     for (int i = gt; i <= W; i += GT) {
       T qm = T(1) / T(i + 1), ql = qm;
       if (qtab) { qm = qtab[2 * i]; ql = qtab[2 * i + 1]; }
@@ -491,7 +496,8 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       const unsigned dv_s = gbase + (unsigned)L.dv, stage_s = gbase + (unsigned)L.stage;
       const unsigned snap_s = gbase + (unsigned)L.snap;
       const unsigned initr_s = gbase + (unsigned)L.initr, ctag_s = gbase + (unsigned)L.ctag;
-      const unsigned fsfin_s = gbase + (unsigned)L.fsfin, bsm_s = gbase + (unsigned)L.bsm;
+      const unsigned fsfin_s = gbase + (unsigned)L.fsfin, tst_s = gbase + (unsigned)L.tst;
+      const unsigned bsm_s = gbase + (unsigned)L.bsm;
       const unsigned qsm_s = gbase + (unsigned)L.qsm, cfin_s = gbase + (unsigned)L.cfin;
       // the background CTA's copies (shared::cluster addresses)
       // the A workers' copy of the final coefficients (shared::cluster address)
@@ -531,6 +537,10 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
         const unsigned dst = stage_s + ((jb & (TC_SRING - 1)) * TC_BT * TC_S + x) * TS;
 #pragma unroll
         for (int i = 0; i < TC_BT; ++i) cp_async_s(dst + i * TC_S * TS, src + i * ld);
+        if (STG && x < TC_BT) {                      // the batch's targets (clamped past the end)
+          const int mi = mb - (TC_BT - 1) + x;
+          cp_async_s(tst_s + ((jb & (TC_SRING - 1)) * TC_BT + x) * TS, B + (mi < Np ? mi : Np - 1));
+        }
         cp_async_commit();
       };
 #pragma unroll 1
@@ -656,7 +666,10 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
         }
         if (!(FEAT & 4)) {
           diag = lds_t<T>(sb + ((rel & (TC_BT - 1)) * TC_S + x) * TS);
-          bt = lds_nv(bsm_s + (unsigned)mt * TS, T(0));
+          if constexpr (STG)
+            bt = lds_t<T>(tst_s + ((jb & (TC_SRING - 1)) * TC_BT + (rel & (TC_BT - 1))) * TS);
+          else
+            bt = lds_nv(bsm_s + (unsigned)mt * TS, T(0));
         }
         mark(2);
         // ---- step n+2: the new slots start from 0; entry check of the next
@@ -1008,19 +1021,19 @@ static int num_sms() {
   return n;
 }
 
-template <typename T, int NG, int CL, int WM>
+template <typename T, int NG, int CL, int WM, bool STG>
 int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long long gram_stride,
                  const T* rx, long long rx_stride, const T* samples, long long samples_stride,
                  int dim, const T* targets, int F, int K, int Np, int W, double eps,
                  kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
                  int* first_step, T* theta, int* n_active, int* status, long long* dbg) {
-  auto kern = apsm_train_kernel<T, NG, CL, WM, false>;
-  if constexpr (sizeof(T) == 4 && NG == 1 && WM == 20) {   // clock instrumentation build
-    if (dbg) kern = apsm_train_kernel<T, NG, CL, WM, true>;
+  auto kern = apsm_train_kernel<T, NG, CL, WM, false, STG>;
+  if constexpr (sizeof(T) == 4 && NG == 1 && WM == 20 && !STG) {   // clock instrumentation build
+    if (dbg) kern = apsm_train_kernel<T, NG, CL, WM, true, false>;
   } else if (dbg) {
     return KAPSM_ERR_UNSUPPORTED;
   }
-  const GroupSmem<T, NG, CL> L(W, Np);
+  const GroupSmem<T, NG, CL> L(W, Np, STG);
   size_t smem = L.total * NG;
   // NG = 1: pad shared memory so that the two CTAs of a cluster land on
   // different SMs (the latency pipeline's concurrent detection screen asks
@@ -1060,12 +1073,20 @@ int launch_train_w(int tasks, cudaStream_t s, const T* gram, long long ld, long 
                    const T* rx, long long rx_stride, const T* samples, long long samples_stride,
                    int dim, const T* targets, int F, int K, int Np, int W, double eps,
                    kapsm_kernel_params p, const T* qtab, const T* base0, const T* theta0, T* coeff,
-                   int* first_step, T* theta, int* n_active, int* status, long long* dbg) {
+                   int* first_step, T* theta, int* n_active, int* status, long long* dbg,
+                   bool stg = false) {
 #define KAPSM_LT(WMV)                                                                          \
-  return launch_train<T, NG, CL, WMV>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples, \
-                                      samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, \
-                                      base0, theta0, coeff, first_step, theta, n_active, status, \
-                                      dbg)
+  do {                                                                                         \
+    if (NG == 1 && stg)                                                                        \
+      return launch_train<T, NG, CL, WMV, true>(tasks, s, gram, ld, gram_stride, rx, rx_stride, \
+                                                samples, samples_stride, dim, targets, F, K, Np, \
+                                                W, eps, p, qtab, base0, theta0, coeff,           \
+                                                first_step, theta, n_active, status, dbg);       \
+    return launch_train<T, NG, CL, WMV, false>(tasks, s, gram, ld, gram_stride, rx, rx_stride,  \
+                                               samples, samples_stride, dim, targets, F, K, Np,  \
+                                               W, eps, p, qtab, base0, theta0, coeff,            \
+                                               first_step, theta, n_active, status, dbg);        \
+  } while (0)
   // the window dot covers the WM newest slots (static per unrolled step)
 #ifdef KAPSM_EXP_ONLY
   if (W == 20) KAPSM_LT(20);
@@ -1106,8 +1127,14 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
       (gram_stride * (long long)sizeof(T)) % 16 || ((size_t)gram & 15))
     return KAPSM_ERR_INVALID;
   const int tasks = F * K;
-  // KAPSM_FORCE_WIDE (tests): the general trainer at any size
-  if (W > TC_MAX_W || Np > TC_MAX_NP || getenv("KAPSM_FORCE_WIDE")) {
+  // the general trainer beyond the latency schedule's window or its
+  // shared-memory footprint (per-sample words in the chain's CTAs), or at any
+  // size with KAPSM_FORCE_WIDE (tests)
+  // targets staged with the columns once the per-sample target array no
+  // longer fits beside the tagged coefficients
+  const bool stg = GroupSmem<T, 1, 2>(W, Np, false).total > 227 * 1024;
+  if (W > TC_MAX_W || Np > TC_MAX_NP || GroupSmem<T, 1, 2>(W, Np, true).total > 227 * 1024 ||
+      getenv("KAPSM_FORCE_WIDE")) {
     if (dbg) return KAPSM_ERR_UNSUPPORTED;
     return train_wide<T>(gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim,
                          targets, F, K, Np, W, eps, p, qtab, base0, theta0, coeff, first_step,
@@ -1117,13 +1144,12 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
   // SMs; throughput mode (4 chains per SM) beyond.  FP64 (the parity/test
   // precision) always runs in latency mode.
   static const bool force_lat = getenv("KAPSM_FORCE_LATENCY_MODE") != nullptr;
-  const bool lat = force_lat || sizeof(T) == 8 || tasks <= num_sms() ||
+  const bool lat = force_lat || stg || sizeof(T) == 8 || tasks <= num_sms() ||
                    GroupSmem<T, 4, 1>(W, Np).total * 4 > 227 * 1024;
-  if (GroupSmem<T, 1, 2>(W, Np).total > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   if (lat)
     return launch_train_w<T, 1, 2>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
                                    samples_stride, dim, targets, F, K, Np, W, eps, p, qtab, base0,
-                                   theta0, coeff, first_step, theta, n_active, status, dbg);
+                                   theta0, coeff, first_step, theta, n_active, status, dbg, stg);
 #ifdef KAPSM_EXP_ONLY
   return KAPSM_ERR_UNSUPPORTED;
 #endif
