@@ -100,8 +100,9 @@ def test_wide_window_sweep_f64(W, n_train, M):
         _check(f, O.train_user(R, B, W=W))
 
 
-def test_wide_many_samples_f64():
-    """Np = 2 n_train > 3072 (C3 n_train rows) against the oracle."""
+def test_many_samples_f64():
+    """Np = 2 n_train = 3200 (beyond the latency trainer's former 3072 limit)
+    against the oracle."""
     n_train = 1600
     fr = O.make_frame(2048, 6, 16, n_train, 8, "QPSK")
     R = O.realify(fr["rx"][:n_train])
@@ -130,4 +131,30 @@ def test_wide_frames_pipeline_large():
     assert not out["f64"][3].any() and not out["f32"][3].any()
     assert np.array_equal(out["f64"][0], out["f32"][0])
     assert np.array_equal(out["f64"][1], out["f32"][1])
+    assert maxrel(out["f32"][2].astype(np.float64), out["f64"][2]) <= 1e-4
+
+
+@pytest.mark.parametrize("n_train", [3500, 6000])
+def test_large_np_paths_agree(n_train):
+    """The latency trainer with staged targets (FP64 at Np = 7000, FP32 at
+    Np = 12000) against the other precision's path (unstaged latency trainer,
+    resp. the general trainer): identical decisions and error counts, soft
+    estimates within 1e-4."""
+    import torch
+    Kk, M, n_data = 2, 16, 256
+    rx, pil, tx, _ = K.host_frames([11], Kk, M, n_train, n_data, "QPSK")
+    out = {}
+    for prec in ("f64", "f32"):
+        p = K.FramePipeline(1, Kk, M, n_train, n_data, "QPSK", precision=prec)
+        p.load(rx, pil, tx)
+        p.launch()
+        torch.cuda.synchronize()
+        out[prec] = (p.labels.cpu().numpy(), p.bit_err.cpu().numpy(), p.est.cpu().numpy(),
+                     p.status.cpu().numpy(), p.n_active.cpu().numpy())
+        del p
+        torch.cuda.empty_cache()
+    assert not out["f64"][3].any() and not out["f32"][3].any()
+    assert np.array_equal(out["f64"][0], out["f32"][0])
+    assert np.array_equal(out["f64"][1], out["f32"][1])
+    assert np.array_equal(out["f64"][4], out["f32"][4])
     assert maxrel(out["f32"][2].astype(np.float64), out["f64"][2]) <= 1e-4
