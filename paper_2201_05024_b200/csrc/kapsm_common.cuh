@@ -352,4 +352,18 @@ template <> KAPSM_DEV void lds_quad<double>(unsigned a, double (&v)[4]) {
   const double2 p = lds_d2(a), q = lds_d2(a + 16);
   v[0] = p.x; v[1] = p.y; v[2] = q.x; v[3] = q.y;
 }
+// Live early Gaussian terms per pilot row (train_wide.cu builds them; both
+// trainers read them): count, then up to KAPSM_LIVE_CAP (column, value) pairs.
+constexpr int KAPSM_LIVE_CAP = 32;
+template <typename T>
+struct LiveLists {
+  void* ws;
+  int* cnt;
+  int* idx;
+  T* val;
+};
+template <typename T>
+int build_live_lists(const T* rx, long long rx_stride, const T* samples, long long samples_stride,
+                     int dim, int F, int Np, int gap, kapsm_kernel_params p, cudaStream_t s,
+                     LiveLists<T>& ll);
 }  // namespace kapsm

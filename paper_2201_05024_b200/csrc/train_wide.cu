@@ -44,7 +44,7 @@ constexpr int TW_Q = 2;                  // band prefetch distance (steps)
 constexpr int TW_R = 16;                 // snapshot ring (>= P + 2, pow2)
 constexpr int TW_HW = 12;                // helper warps
 constexpr int TW_TR = 16;                // theta ring (>= P + E + 2)
-constexpr int TW_LCAP = 32;              // live early Gaussian terms kept per row
+constexpr int TW_LCAP = KAPSM_LIVE_CAP;  // live early Gaussian terms kept per row
 constexpr int TW_MAX_DIM = 128;          // realified dimension (theta in registers)
 constexpr int TW_MAX_LATE = 160;         // late-part terms W + E (registers)
 constexpr int TW_MAX_THREADS = 640;
@@ -542,6 +542,37 @@ __global__ void __launch_bounds__(256)
       if (m0 + warp * 4 + r < Np) cnt[m0 + warp * 4 + r] = c[r];
 }
 
+// Live lists of every pilot row (l <= m - gap) in stream-ordered scratch
+// memory (cudaMallocAsync; free with cudaFreeAsync(ll.ws) on the same stream).
+template <typename T>
+int build_live_lists(const T* rx, long long rx_stride, const T* samples, long long samples_stride,
+                     int dim, int F, int Np, int gap, kapsm_kernel_params p, cudaStream_t s,
+                     LiveLists<T>& ll) {
+  const size_t rows = (size_t)F * Np;
+  const size_t b_cnt = (rows * sizeof(int) + 255) & ~size_t(255);
+  const size_t b_idx = (rows * TW_LCAP * sizeof(int) + 255) & ~size_t(255);
+  const size_t b_val = rows * TW_LCAP * sizeof(T);
+  ll.ws = nullptr;
+  if (cudaMallocAsync(&ll.ws, b_cnt + b_idx + b_val, s) != cudaSuccess) return KAPSM_ERR_CUDA;
+  ll.cnt = static_cast<int*>(ll.ws);
+  ll.idx = reinterpret_cast<int*>(static_cast<char*>(ll.ws) + b_cnt);
+  ll.val = reinterpret_cast<T*>(static_cast<char*>(ll.ws) + b_cnt + b_idx);
+  const size_t lsm = 2 * 32 * (size_t)(dim + 1) * sizeof(T);
+  if (cudaFuncSetAttribute(live_lists_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)lsm) != cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  live_lists_kernel<T><<<dim3((Np + 31) / 32, F), 256, lsm, s>>>(
+      rx, rx_stride, samples, samples_stride, dim, Np, gap, (T)p.w_g,
+      (T)(1.0 / (2.0 * p.sigma_sq)), ll.cnt, ll.idx, ll.val);
+  return status_from(cudaGetLastError());
+}
+template int build_live_lists<float>(const float*, long long, const float*, long long, int, int,
+                                     int, int, kapsm_kernel_params, cudaStream_t,
+                                     LiveLists<float>&);
+template int build_live_lists<double>(const double*, long long, const double*, long long, int,
+                                      int, int, int, kapsm_kernel_params, cudaStream_t,
+                                      LiveLists<double>&);
+
 static int wide_num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -569,26 +600,13 @@ int train_wide(const T* gram, long long ld, long long gram_stride, const T* rx,
       cudaSuccess)
     return KAPSM_ERR_CUDA;
   // live-term lists (stream-ordered scratch: F x Np rows)
-  const size_t rows = (size_t)F * Np;
-  const size_t b_cnt = (rows * sizeof(int) + 255) & ~size_t(255);
-  const size_t b_idx = (rows * TW_LCAP * sizeof(int) + 255) & ~size_t(255);
-  const size_t b_val = rows * TW_LCAP * sizeof(T);
-  void* ws = nullptr;
-  if (cudaMallocAsync(&ws, b_cnt + b_idx + b_val, s) != cudaSuccess) return KAPSM_ERR_CUDA;
-  int* lcnt = static_cast<int*>(ws);
-  int* lidx = reinterpret_cast<int*>(static_cast<char*>(ws) + b_cnt);
-  T* lval = reinterpret_cast<T*>(static_cast<char*>(ws) + b_cnt + b_idx);
-  const size_t lsm = 2 * 32 * (size_t)(dim + 1) * sizeof(T);
-  int r = KAPSM_OK;
-  if (cudaFuncSetAttribute(live_lists_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)lsm) != cudaSuccess)
-    r = KAPSM_ERR_CUDA;
-  if (r == KAPSM_OK) {
-    live_lists_kernel<T><<<dim3((Np + 31) / 32, F), 256, lsm, s>>>(
-        rx, rx_stride, samples, samples_stride, dim, Np, TW_P + 1 + W + TW_E, (T)p.w_g,
-        (T)(1.0 / (2.0 * p.sigma_sq)), lcnt, lidx, lval);
-    r = status_from(cudaGetLastError());
-  }
+  LiveLists<T> ll;
+  int r = build_live_lists<T>(rx, rx_stride, samples, samples_stride, dim, F, Np,
+                              TW_P + 1 + W + TW_E, p, s, ll);
+  int* lcnt = ll.cnt;
+  int* lidx = ll.idx;
+  T* lval = ll.val;
+  void* ws = ll.ws;
   if (r == KAPSM_OK) {
     const int tasks = F * K;
     const int grid = tasks < wide_num_sms() ? tasks : wide_num_sms();

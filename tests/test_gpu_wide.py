@@ -158,3 +158,17 @@ def test_large_np_paths_agree(n_train):
     assert np.array_equal(out["f64"][1], out["f32"][1])
     assert np.array_equal(out["f64"][4], out["f32"][4])
     assert maxrel(out["f32"][2].astype(np.float64), out["f64"][2]) <= 1e-4
+
+
+def test_large_np_latency_trainer_f64_vs_oracle():
+    """Np = 4200 > 4096: the latency trainer's early parts come from the running
+    linear part + live Gaussian lists (no Gram row streaming) -- FP64 against
+    the oracle."""
+    n_train = 2100
+    fr = O.make_frame(4200, 6, 16, n_train, 8, "QPSK")
+    R = O.realify(fr["rx"][:n_train])
+    u = 1
+    B = O.realify_targets(fr["symbols"][u, :n_train])
+    f = K.train(None, zip(fr["rx"][:n_train], fr["symbols"][u, :n_train]), K.ApsmConfig(),
+                precision="f64")
+    _check(f, O.train_user(R, B, W=20))
