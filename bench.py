@@ -358,10 +358,14 @@ def main():
 
     lab_g = None
 
+    # N > 1: one exchange step per 16 frames per rank (decisions all-gathered,
+    # error counters all-reduced), serialized on the FrameStream's collective stream
+    exchanges = {}
+
     def post(pp):
-        if world > 1:
-            D.gather_decisions(pp.labels)
-            D.reduce_counts(pp.bit_err)
+        if "ex" not in exchanges:
+            exchanges["ex"] = D.BatchedExchange(16, (K_USERS, N_DATA), dev)
+        exchanges["ex"].add(pp.labels, torch.cat([pp.bit_err[0], pp.sym_err[0]]))
 
     # device-resident steps: the pool frame is copied into one of two captured
     # pipelines on a copy stream while the previous frame computes (FrameStream)

@@ -20,7 +20,8 @@ from typing import Optional, Sequence
 import torch
 import torch.distributed as tdist
 
-__all__ = ["RankInfo", "init_from_env", "shard_frames", "gather_decisions", "reduce_counts"]
+__all__ = ["RankInfo", "init_from_env", "shard_frames", "gather_decisions", "reduce_counts",
+           "BatchedExchange"]
 
 
 @dataclass(frozen=True)
@@ -79,3 +80,36 @@ def reduce_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
     if tdist.is_initialized() and tdist.get_world_size(group) > 1:
         tdist.all_reduce(counts, op=tdist.ReduceOp.SUM, group=group)
     return counts
+
+
+class BatchedExchange:
+    """One exchange step per batch of frames: each rank stages
+    its frames' decisions into a (batch, K, n_data) buffer and accumulates
+    their error counters; every ``batch`` frames the buffer is all-gathered
+    and the counters all-reduced (two collectives per batch instead of per
+    frame).  Every rank must call ``add`` the same number of times.  Runs on
+    the caller's current stream (CUDA) or on CPU tensors (gloo)."""
+
+    def __init__(self, batch: int, labels_shape, device, group=None):
+        if batch < 1:
+            raise ValueError(f"batch must be >= 1, got {batch}")
+        self.batch, self.group = batch, group
+        self.buf = torch.zeros((batch,) + tuple(labels_shape), dtype=torch.uint8, device=device)
+        self.acc = None
+        self.n = 0
+        self.gathered = None          # last batch: (world, batch, ...) decisions
+        self.totals = None            # last batch: summed counters
+
+    def add(self, labels: torch.Tensor, counts: torch.Tensor):
+        k = self.n % self.batch
+        self.buf[k].copy_(labels.reshape(self.buf.shape[1:]))
+        if self.acc is None:
+            self.acc = torch.zeros_like(counts)
+        self.acc.add_(counts)
+        self.n += 1
+        if self.n % self.batch == 0:
+            self.gathered = gather_decisions(self.buf, self.group)
+            self.totals = reduce_counts(self.acc.clone(), self.group)
+            self.acc.zero_()
+            return True
+        return False

@@ -30,9 +30,16 @@ def _worker(rank, world, port, q):
         g = D.gather_decisions(labels)
         counts = torch.tensor([[rank, 10 * rank, 1]], dtype=torch.int64)
         D.reduce_counts(counts)
-        q.put((rank, frames, tuple(g.shape), g[:, 0, 0, 0].tolist(), counts.tolist()))
+        # batched exchange: 5 frames per rank, batches of 2 -> 2 exchange steps
+        ex = D.BatchedExchange(2, (K, nd), "cpu")
+        steps = 0
+        for fi in range(5):
+            lab = torch.full((1, K, nd), 10 * rank + fi, dtype=torch.uint8)
+            steps += ex.add(lab, torch.tensor([1, rank], dtype=torch.int64))
+        bx = (steps, tuple(ex.gathered.shape), ex.gathered[:, :, 0, 0].tolist(), ex.totals.tolist())
+        q.put((rank, frames, tuple(g.shape), g[:, 0, 0, 0].tolist(), counts.tolist(), bx))
       except Exception as e:  # report instead of hanging the parent
-        q.put((rank, "error", repr(e), None, None))
+        q.put((rank, "error", repr(e), None, None, None))
     finally:
         if tdist.is_initialized():
             tdist.destroy_process_group()
@@ -58,8 +65,10 @@ def test_gather_and_reduce_world2_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, f0, s0, v0, c0), (r1, f1, s1, v1, c1) = res
+    (r0, f0, s0, v0, c0, b0), (r1, f1, s1, v1, c1, b1) = res
     assert f0 == [0, 2, 4, 6, 8] and f1 == [1, 3, 5, 7, 9]
     assert tuple(s0) == (2, 5, 3, 5)
     assert v0 == [1, 2] and v1 == [1, 2]
     assert c0 == c1 == [[1, 10, 2]]
+    # last exchanged batch = frames 2, 3 of each rank; counters summed over 2 frames x 2 ranks
+    assert b0 == b1 == (2, (2, 2, 3, 5), [[2, 3], [12, 13]], [4, 2])

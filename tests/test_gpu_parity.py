@@ -410,3 +410,28 @@ def test_frame_stream_matches_pipeline():
         r = ref.results(est=False)
         assert np.array_equal(lab.numpy(), r["labels"])
         assert np.array_equal(be.numpy(), r["bit_err"]) and np.array_equal(se.numpy(), r["sym_err"])
+
+
+def test_frame_stream_batched_exchange_hook():
+    """The N > 1 bench hook at world 1: BatchedExchange on the FrameStream's
+    collective stream sees every frame's decisions and counters in order."""
+    import torch
+    from paper_2201_05024_b200 import dist as D
+    Kk, M, nt, nd = 3, 8, 120, 200
+    rx, pil, tx, _ = K.host_frames(range(8), Kk, M, nt, nd, "QPSK")
+    rx_p = torch.from_numpy(np.stack([rx.real, rx.imag], -1).astype(np.float32)).pin_memory()
+    pil_p = torch.from_numpy(np.stack([pil.real, pil.imag], -1).astype(np.float32)).pin_memory()
+    tx_p = torch.from_numpy(tx.astype(np.uint8)).pin_memory()
+    ex = D.BatchedExchange(4, (Kk, nd), torch.device("cuda"))
+    fs = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=3, concurrent=True,
+                       post=lambda p: ex.add(p.labels, torch.cat([p.bit_err[0], p.sym_err[0]])))
+    labs, errs = [], []
+    for i in range(8):
+        t = fs.submit(rx_p[i:i + 1], pil_p[i:i + 1], tx_p[i:i + 1])
+        lab, be, se = fs.result(t)
+        labs.append(lab.clone())
+        errs.append(torch.cat([be[0], se[0]]).clone())
+    torch.cuda.synchronize()
+    assert ex.n == 8
+    assert np.array_equal(ex.gathered[0].cpu().numpy(), torch.cat(labs[4:]).numpy())
+    assert np.array_equal(ex.totals.cpu().numpy(), sum(e.numpy() for e in errs[4:]))
