@@ -314,7 +314,7 @@ def main():
     # (tests/golden/c1_s0_users01.npz, written by the unmodified reference):
     # soft estimates within 1e-4, bit-error counts and atom counts identical.
     gate = None
-    if rank == 0:
+    if True:                       # every rank (a failure must stop all of them)
         gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden",
                              "c1_s0_users01.npz")
         g = np.load(gpath)
@@ -333,7 +333,8 @@ def main():
                 "counts_identical": bool(same), "pass": bool(same and worst <= 1e-4)}
         del gp
         if not gate["pass"]:
-            emit({"metric": METRIC, "error": "correctness gate failed", "gate": gate})
+            if rank == 0:
+                emit({"metric": METRIC, "error": "correctness gate failed", "gate": gate})
             return 1
 
     # ---------------- frame pool (distinct seeds per rank, > L2) ----------------
