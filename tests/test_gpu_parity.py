@@ -435,3 +435,26 @@ def test_frame_stream_batched_exchange_hook():
     assert ex.n == 8
     assert np.array_equal(ex.gathered[0].cpu().numpy(), torch.cat(labs[4:]).numpy())
     assert np.array_equal(ex.totals.cpu().numpy(), sum(e.numpy() for e in errs[4:]))
+
+
+def test_launch_on_device_frames_in_place():
+    """FramePipeline.launch_on reads device-resident frames in place (no copy
+    into the static buffers) and matches load + launch; bad tensors raise."""
+    import torch
+    Kk, M, nt, nd = 3, 8, 120, 200
+    rx, pil, tx, _ = K.host_frames([21], Kk, M, nt, nd, "QPSK")
+    p = K.FramePipeline(1, Kk, M, nt, nd, "QPSK", precision="f32")
+    p.load(rx, pil, tx)
+    p.launch()
+    ref = p.results(est=True)
+    rx_d = torch.from_numpy(np.stack([rx.real, rx.imag], -1).astype(np.float32)).cuda()
+    pil_d = torch.from_numpy(np.stack([pil.real, pil.imag], -1).astype(np.float32)).cuda()
+    tx_d = torch.from_numpy(tx.astype(np.uint8)).cuda()
+    q = K.FramePipeline(1, Kk, M, nt, nd, "QPSK", precision="f32")
+    q.launch_on(rx_d, pil_d, tx_d)
+    got = q.results(est=True)
+    assert np.array_equal(got["labels"], ref["labels"])
+    assert np.array_equal(got["bit_err"], ref["bit_err"])
+    assert np.array_equal(got["est"], ref["est"])
+    with pytest.raises(ValueError):
+        q.launch_on(rx_d.double(), pil_d, tx_d)
