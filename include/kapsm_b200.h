@@ -152,6 +152,25 @@ int kapsm_train_f64(const double* gram, long long ld, long long gram_stride, con
                     const double* base0, const double* theta0, double* coeff, int* first_step,
                     double* theta, int* n_active, int* status, void* stream);
 
+/* The general trainer (train_wide.cu) at any size: same arguments and
+ * results as kapsm_train_*, which selects it by itself beyond the latency
+ * kernel's window / shared-memory limits.  Exported so its parity can be
+ * tested on the small golden frames. */
+int kapsm_train_general_f32(const float* gram, long long ld, long long gram_stride,
+                            const float* rx, long long rx_stride, const float* samples,
+                            long long samples_stride, int dim, const float* targets, int F, int K,
+                            int n_samples, int window, double epsilon, kapsm_kernel_params p,
+                            const float* qtab, const float* base0, const float* theta0,
+                            float* coeff, int* first_step, float* theta, int* n_active,
+                            int* status, void* stream);
+int kapsm_train_general_f64(const double* gram, long long ld, long long gram_stride,
+                            const double* rx, long long rx_stride, const double* samples,
+                            long long samples_stride, int dim, const double* targets, int F,
+                            int K, int n_samples, int window, double epsilon,
+                            kapsm_kernel_params p, const double* qtab, const double* base0,
+                            const double* theta0, double* coeff, int* first_step, double* theta,
+                            int* n_active, int* status, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K3  Fused frame detection.
  * Replaces batch_detect / batch_evaluate (engine.py:206-261) for the filters

@@ -18,10 +18,13 @@ is missing.
 from .apsm import (ApsmConfig, ApsmTrainer, DegenerateSampleError, DictionaryCapacityError,
                    TrainingSample, apsm_step, beta, complex_to_real_pair, detect_symbol,
                    realify_batch, train, uniform_weights, window_indices)
+from .bench import BenchReport, BenchRow, bench_detection, report_to_csv, report_to_json
 from .engine import STAGES, EngineConfig, batch_detect, batch_evaluate
 from .frames import FramePipeline, FrameStream, host_frames
-from .kernels import (FilterState, KernelParams, evaluate, from_expansion, inner_product, norm_sq,
-                      self_kernel, zero_filter)
+from .kernels import (FilterState, KernelParams, evaluate, from_expansion, inner_product,
+                      kernel_gaussian, kernel_linear, kernel_sum, norm_sq, self_kernel, zero_filter)
+from .modelio import (IQ_MAGIC, MODEL_MAGIC, FileFormatError, load_iq, load_model, load_symbols,
+                      save_iq, save_model, save_symbols)
 from .noma import (SCHEMES, ChannelModel, Constellation, FrameSpec, TrialReport, ber,
                    demodulate_hard, draw_channel, get_constellation, modulate, noise_var_for_snr,
                    run_trial, seeded_frame, symbol_labels, synthesize_received)

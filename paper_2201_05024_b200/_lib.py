@@ -13,8 +13,6 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libkapsm_b200.so")
-# developer knob (kernel experiments): load another build of the same C ABI
-LIB_PATH = os.environ.get("KAPSM_LIB_PATH", LIB_PATH)
 
 KAPSM_OK = 0
 KAPSM_ERR_INVALID = 1
@@ -48,6 +46,10 @@ SIGNATURES = {
                              _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "kapsm_train_f64": (_I, [_P, _LL, _LL, _P, _LL, _P, _LL, _I, _P, _I, _I, _I, _I, _D, _KP,
                              _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "kapsm_train_general_f32": (_I, [_P, _LL, _LL, _P, _LL, _P, _LL, _I, _P, _I, _I, _I, _I, _D,
+                                     _KP, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "kapsm_train_general_f64": (_I, [_P, _LL, _LL, _P, _LL, _P, _LL, _I, _P, _I, _I, _I, _I, _D,
+                                     _KP, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "kapsm_detect_frames_f32": (_I, [_P, _LL, _I, _I, _I, _I, _I, _P, _P, _KP, _P, _I, _I, _P,
                                      _P, _P, _P, _P, _P]),
     "kapsm_detect_frames_f64": (_I, [_P, _LL, _I, _I, _I, _I, _I, _P, _P, _KP, _P, _I, _I, _P,

@@ -198,6 +198,12 @@ def _ld(n: int) -> int:
     return (n + 16 + 31) // 32 * 32
 
 
+# C-ABI trainer entry: "kapsm_train" picks the latency kernel or the general
+# trainer by window / size; tests point it at "kapsm_train_general" to check
+# the general trainer on the small golden frames.
+_TRAIN_ENTRY = "kapsm_train"
+
+
 def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,
                   samples=None, targets_r=None, f0: Optional[FilterState] = None):
     """Run K1 + K2 for one (frame, user).
@@ -249,7 +255,7 @@ def _train_device(cfg: ApsmConfig, prec: str, *, rx_pilots=None, targets_c=None,
     nact = torch.empty((1,), dtype=torch.int32, device=dv.device())
     status = torch.empty((1,), dtype=torch.int32, device=dv.device())
     q = qtab_device(cfg.window, prec)
-    _lib.check(dv.fn("kapsm_train", prec)(
+    _lib.check(dv.fn(_TRAIN_ENTRY, prec)(
         dv.ptr(gram), ld, N * ld,
         dv.ptr(rxd) if rx_pilots is not None else dv.ptr(None), N * M if rx_pilots is not None else 0,
         dv.ptr(sd) if rx_pilots is None else dv.ptr(None), N * D if rx_pilots is None else 0,
@@ -289,8 +295,12 @@ class ApsmTrainer:
     ``observe`` validates and buffers the realified sample (shape and
     degenerate-sample errors are raised immediately, as in the reference);
     ``state`` runs the persistent GPU trainer over the buffered stream and
-    returns the identical FilterState.  DictionaryCapacityError is raised by
-    ``state`` (the reference raises it from the observe that crosses the cap).
+    returns the identical FilterState.  With a ``max_atoms`` cap,
+    DictionaryCapacityError comes from the observe that crosses the cap, as
+    in apsm.py:341-349: every sample owns at most one slot, so while
+    ``f0.n_atoms + n_seen <= max_atoms`` no observe can cross it; past that
+    point each observe runs the chain over the buffered stream (one launch)
+    and raises if the slot count passes the cap.
     """
 
     def __init__(self, dim: int, cfg: ApsmConfig, f0: Optional[FilterState] = None,
@@ -326,6 +336,9 @@ class ApsmTrainer:
         self._rows.append(r.copy())
         self._targets.append(float(b))
         self._cache = None
+        cap = self.cfg.max_atoms
+        if cap is not None and p.w_g != 0.0 and self.f0.n_atoms + len(self._rows) > cap:
+            self.state()            # raises DictionaryCapacityError past the cap
 
     def observe_symbol(self, r, b):
         s1, s2 = complex_to_real_pair(r, b)

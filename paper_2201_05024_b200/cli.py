@@ -4,6 +4,12 @@ commands of the reference CLI (kapsm/cli.py:168-198) on the GPU path.
     train  --iq CAPTURE --pilots SYMBOLS --out MODEL [--window W --epsilon E
            --w-l --w-g --sigma-sq --precision f64|f32]
     detect MODEL CAPTURE OUT [--precision f32|f64]
+    bench  [--dict-sizes ... --batch-sizes ... --stages ... --workers ...
+           --repeats R --seed S --antennas M --precision --json --out FILE]
+
+``bench`` is the reference's ``kapsm bench`` (cli.py:144-165): the detection
+harness (bench.py here) with B200 rows, CSV or JSON on stdout / --out, exit 1
+when a row fails the checksum gate.
 
 Training runs the persistent GPU trainer on the first len(pilots) samples of
 the capture; detection runs the GPU evaluation engine and writes float32
@@ -19,6 +25,7 @@ import argparse
 import sys
 
 from .apsm import ApsmConfig, train
+from .bench import bench_detection, report_to_csv, report_to_json
 from .engine import EngineConfig, batch_detect
 from .kernels import KernelParams, zero_filter
 from .modelio import FileFormatError, load_iq, load_model, load_symbols, save_model, save_symbols
@@ -50,6 +57,25 @@ def _detect(a) -> int:
     return 0
 
 
+def _bench(a) -> int:
+    rep = bench_detection(a.dict_sizes, a.batch_sizes, a.stages, a.workers, a.repeats,
+                          seed=a.seed, antennas=a.antennas,
+                          params=KernelParams(a.w_l, a.w_g, a.sigma_sq),
+                          engine_template=EngineConfig(precision=a.precision))
+    text = report_to_json(rep) if a.json else report_to_csv(rep)
+    if a.out:
+        with open(a.out, "w") as fh:
+            fh.write(text)
+    else:
+        sys.stdout.write(text)
+    if rep.has_failures:
+        bad = sorted({r.stage for r in rep.rows if not r.ok})
+        print(f"error: checksum mismatch against baseline for stage(s): {', '.join(bad)}",
+              file=sys.stderr)
+        return 1
+    return 0
+
+
 def _parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="kapsm_b200",
                                  description="APSM multiuser detector on B200: file-based "
@@ -72,6 +98,21 @@ def _parser() -> argparse.ArgumentParser:
     d.add_argument("out")
     d.add_argument("--precision", choices=("f64", "f32"), default="f64")
     d.set_defaults(func=_detect)
+    b = sub.add_parser("bench", help="detection latency harness (checksum-gated rows)")
+    b.add_argument("--dict-sizes", type=int, nargs="+", default=[10_000])
+    b.add_argument("--batch-sizes", type=int, nargs="+", default=[4_096])
+    b.add_argument("--stages", nargs="+", default=["baseline", "tiled", "balanced"])
+    b.add_argument("--workers", type=int, nargs="+", default=[1])
+    b.add_argument("--repeats", type=int, default=5)
+    b.add_argument("--seed", type=int, default=0)
+    b.add_argument("--antennas", type=int, default=16)
+    b.add_argument("--w-l", type=float, default=0.5)
+    b.add_argument("--w-g", type=float, default=0.5)
+    b.add_argument("--sigma-sq", type=float, default=0.05)
+    b.add_argument("--precision", choices=("f64", "f32"), default="f64")
+    b.add_argument("--json", action="store_true")
+    b.add_argument("--out")
+    b.set_defaults(func=_bench)
     return ap
 
 

@@ -337,12 +337,9 @@ int detect_frames(const T* rx, long long rx_stride, int F, int K, int n_train, i
   if (M <= 4) KAPSM_DK(4);
   if (M <= 8) KAPSM_DK(8);
   if (M <= 16) KAPSM_DK(16);
-  if constexpr (sizeof(T) == 4) {
-    if (M <= 32) KAPSM_DK(32);
-    if (M <= 64) KAPSM_DK(64);
-  } else {
-    if (M <= 32) KAPSM_DK(32);
-  }
+  if (M <= 32) KAPSM_DK(32);
+  if (M <= 64) KAPSM_DK(64);       // FP64 at M = 64 spills its row registers: the
+                                   // parity twin of the C4 config, not a fast path
 #undef KAPSM_DK
   return KAPSM_ERR_UNSUPPORTED;
 }
@@ -432,8 +429,7 @@ int batch_evaluate(const T* theta, const T* atoms, const T* coeffs, int n_atoms,
   if (dim <= 16) return launch_evaluate<T, 16>(theta, atoms, coeffs, n_atoms, dim, inputs, n_inputs, p, out, s);
   if (dim <= 32) return launch_evaluate<T, 32>(theta, atoms, coeffs, n_atoms, dim, inputs, n_inputs, p, out, s);
   if (dim <= 64) return launch_evaluate<T, 64>(theta, atoms, coeffs, n_atoms, dim, inputs, n_inputs, p, out, s);
-  if constexpr (sizeof(T) == 4)
-    if (dim <= 128) return launch_evaluate<T, 128>(theta, atoms, coeffs, n_atoms, dim, inputs, n_inputs, p, out, s);
+  if (dim <= 128) return launch_evaluate<T, 128>(theta, atoms, coeffs, n_atoms, dim, inputs, n_inputs, p, out, s);
   return KAPSM_ERR_UNSUPPORTED;
 }
 
@@ -524,8 +520,7 @@ int batch_detect(const T* theta, const T* atoms, const T* coeffs, int n_atoms, i
   if (M <= 8) return launch_detect_complex<T, 8>(theta, atoms, coeffs, n_atoms, M, rx, n, p, out, s);
   if (M <= 16) return launch_detect_complex<T, 16>(theta, atoms, coeffs, n_atoms, M, rx, n, p, out, s);
   if (M <= 32) return launch_detect_complex<T, 32>(theta, atoms, coeffs, n_atoms, M, rx, n, p, out, s);
-  if constexpr (sizeof(T) == 4)
-    if (M <= 64) return launch_detect_complex<T, 64>(theta, atoms, coeffs, n_atoms, M, rx, n, p, out, s);
+  if (M <= 64) return launch_detect_complex<T, 64>(theta, atoms, coeffs, n_atoms, M, rx, n, p, out, s);
   return KAPSM_ERR_UNSUPPORTED;
 }
 

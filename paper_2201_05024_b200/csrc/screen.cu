@@ -400,8 +400,7 @@ int screen(const T* rx, long long rx_stride, int F, int n_train, int n_data, int
   if (M <= 8) return launch_screen<T, 8>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
   if (M <= 16) return launch_screen<T, 16>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
   if (M <= 32) return launch_screen<T, 32>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
-  if constexpr (sizeof(T) == 4)
-    if (M <= 64) return launch_screen<T, 64>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
+  if (M <= 64) return launch_screen<T, 64>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
   return KAPSM_ERR_UNSUPPORTED;
 }
 
@@ -422,8 +421,7 @@ int finish(const T* rx, long long rx_stride, int F, int K, int n_train, int n_da
   if (M <= 8) KAPSM_FM(8);
   if (M <= 16) KAPSM_FM(16);
   if (M <= 32) KAPSM_FM(32);
-  if constexpr (sizeof(T) == 4)
-    if (M <= 64) KAPSM_FM(64);
+  if (M <= 64) KAPSM_FM(64);
 #undef KAPSM_FM
   return KAPSM_ERR_UNSUPPORTED;
 }

@@ -1046,8 +1046,6 @@ int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long lo
   int groups = (tasks + NG - 1) / NG;                 // CTAs (CL = 1) or clusters (CL = 2)
   const int max_groups = num_sms() / CL;
   if (groups > max_groups) groups = max_groups;
-  if (const char* cap = getenv("KAPSM_GRID_CAP"))
-    if (atoi(cap) > 0 && groups > atoi(cap)) groups = atoi(cap);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * CL);
   cfg.blockDim = dim3(Roles<NG, CL>::WARPS * 32);
@@ -1115,7 +1113,7 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
           const T* samples, long long samples_stride, int dim, const T* targets, int F, int K,
           int Np, int W, double eps, kapsm_kernel_params p, const T* qtab, const T* base0,
           const T* theta0, T* coeff, int* first_step, T* theta, int* n_active, int* status,
-          cudaStream_t s, long long* dbg = nullptr) {
+          cudaStream_t s, long long* dbg = nullptr, bool general = false) {
   if (F < 0 || K < 1 || Np < 1 || dim < 1 || W < 1 || !(eps > 0)) return KAPSM_ERR_INVALID;
   if (F == 0) return KAPSM_OK;
   if (!gram || !targets || !coeff || !first_step || !theta || !n_active || !status)
@@ -1129,12 +1127,12 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
   const int tasks = F * K;
   // the general trainer beyond the latency schedule's window or its
   // shared-memory footprint (per-sample words in the chain's CTAs), or at any
-  // size with KAPSM_FORCE_WIDE (tests)
+  // size through kapsm_train_general_* (parity tests of that kernel)
   // targets staged with the columns once the per-sample target array no
   // longer fits beside the tagged coefficients
   const bool stg = GroupSmem<T, 1, 2>(W, Np, false).total > 227 * 1024;
   if (W > TC_MAX_W || Np > TC_MAX_NP || GroupSmem<T, 1, 2>(W, Np, true).total > 227 * 1024 ||
-      getenv("KAPSM_FORCE_WIDE")) {
+      general) {
     if (dbg) return KAPSM_ERR_UNSUPPORTED;
     return train_wide<T>(gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim,
                          targets, F, K, Np, W, eps, p, qtab, base0, theta0, coeff, first_step,
@@ -1143,8 +1141,7 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
   // latency mode (a 2-CTA cluster per chain) while the chains fit twice on the
   // SMs; throughput mode (4 chains per SM) beyond.  FP64 (the parity/test
   // precision) always runs in latency mode.
-  static const bool force_lat = getenv("KAPSM_FORCE_LATENCY_MODE") != nullptr;
-  const bool lat = force_lat || stg || sizeof(T) == 8 || tasks <= num_sms() ||
+  const bool lat = stg || sizeof(T) == 8 || tasks <= num_sms() ||
                    GroupSmem<T, 4, 1>(W, Np).total * 4 > 227 * 1024;
   if (lat)
     return launch_train_w<T, 1, 2>(tasks, s, gram, ld, gram_stride, rx, rx_stride, samples,
@@ -1180,6 +1177,21 @@ extern "C" int kapsm_max_samples(void) { return 1 << 20; }
   }
 KAPSM_TRAIN_ENTRY(kapsm_train_f32, float)
 KAPSM_TRAIN_ENTRY(kapsm_train_f64, double)
+
+#define KAPSM_TRAIN_GENERAL_ENTRY(NAME, T)                                                     \
+  extern "C" int NAME(const T* gram, long long ld, long long gram_stride, const T* rx,         \
+                      long long rx_stride, const T* samples, long long samples_stride, int dim, \
+                      const T* targets, int F, int K, int n_samples, int window,               \
+                      double epsilon, kapsm_kernel_params p, const T* qtab, const T* base0,    \
+                      const T* theta0, T* coeff, int* first_step, T* theta, int* n_active,     \
+                      int* status, void* stream) {                                             \
+    return kapsm::train<T>(gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, \
+                           targets, F, K, n_samples, window, epsilon, p, qtab, base0, theta0,  \
+                           coeff, first_step, theta, n_active, status, (cudaStream_t)stream,   \
+                           nullptr, true);                                                     \
+  }
+KAPSM_TRAIN_GENERAL_ENTRY(kapsm_train_general_f32, float)
+KAPSM_TRAIN_GENERAL_ENTRY(kapsm_train_general_f64, double)
 
 // Internal instrumentation entry (not part of the public ABI): as
 // kapsm_train_f32, plus clock64() at the top of every step of (frame 0, user 0).

@@ -68,7 +68,7 @@ def gather_decisions(labels: torch.Tensor, group=None) -> torch.Tensor:
     """All ranks' decision tensors stacked along a new leading rank axis."""
     world = tdist.get_world_size(group) if tdist.is_initialized() else 1
     if world == 1:
-        return labels.unsqueeze(0)
+        return labels.unsqueeze(0).clone()
     x = labels.contiguous()
     out = torch.empty((world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
     tdist.all_gather_into_tensor(out, x, group=group)
@@ -108,8 +108,27 @@ class BatchedExchange:
         self.acc.add_(counts)
         self.n += 1
         if self.n % self.batch == 0:
-            self.gathered = gather_decisions(self.buf, self.group)
-            self.totals = reduce_counts(self.acc.clone(), self.group)
-            self.acc.zero_()
+            self._exchange(self.batch)
             return True
         return False
+
+    @property
+    def pending(self) -> int:
+        """Frames added since the last exchange."""
+        return self.n % self.batch
+
+    def flush(self) -> bool:
+        """Exchange a trailing partial batch (every rank must call it after
+        the same number of ``add``s).  ``gathered`` then holds only the
+        pending frames: shape (world, pending, ...)."""
+        k = self.pending
+        if k == 0:
+            return False
+        self._exchange(k)
+        self.n += self.batch - k          # the next add starts a fresh batch
+        return True
+
+    def _exchange(self, k: int):
+        self.gathered = gather_decisions(self.buf[:k].contiguous(), self.group)
+        self.totals = reduce_counts(self.acc.clone(), self.group)
+        self.acc.zero_()

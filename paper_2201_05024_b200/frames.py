@@ -144,44 +144,13 @@ class FramePipeline:
         else:
             _lib.check(self._fn(*args, dv.stream()), "run_frames")
 
-    def launch(self, time_detect: bool = False):
-        """Enqueue the whole pipeline on the current stream.  With time_detect,
-        run the stages separately and return the detection kernel time in us."""
-        if not time_detect:
-            if self.overlap:
-                _lib.check(self._fn(*self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
-                           "run_frames_overlap")
-            else:
-                _lib.check(self._fn(*self._args(), dv.stream()), "run_frames")
-            return None
-        lib = _lib.load()
-        c = self.cfg
-        p = _lib.params(c.params)
-        st = dv.stream()
-        pre = self.prec
-        self.bit_err.zero_()
-        self.sym_err.zero_()
-        gstride = self.Np * self.ld
-        _lib.check(dv.fn("kapsm_pilot_gram", pre)(dv.ptr(self.rx), self.T * self.M * 2, self.F,
-                                                  self.n_train, self.M, p, dv.ptr(self.gram),
-                                                  self.ld, gstride, st), "pilot_gram")
-        _lib.check(dv.fn("kapsm_train", pre)(
-            dv.ptr(self.gram), self.ld, gstride, dv.ptr(self.rx), self.T * self.M * 2,
-            dv.ptr(None), 0, 2 * self.M, dv.ptr(self.pilots), self.F, self.K, self.Np, c.window,
-            float(c.epsilon), p, dv.ptr(self.qtab), dv.ptr(None), dv.ptr(None),
-            dv.ptr(self.coeff), dv.ptr(self.first_step), dv.ptr(self.theta),
-            dv.ptr(self.n_active), dv.ptr(self.status), st), "train")
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _lib.check(dv.fn("kapsm_detect_frames", pre)(
-            dv.ptr(self.rx), self.T * self.M * 2, self.F, self.K, self.n_train, self.n_data,
-            self.M, dv.ptr(self.coeff), dv.ptr(self.theta), p, dv.ptr(self.points),
-            self.n_points, self.bps, dv.ptr(self.tx), dv.ptr(self.est), dv.ptr(self.labels),
-            dv.ptr(self.bit_err), dv.ptr(self.sym_err), st), "detect_frames")
-        e1.record()
-        e1.synchronize()
-        del lib
-        return e0.elapsed_time(e1) * 1e3
+    def launch(self):
+        """Enqueue the whole pipeline on the current stream."""
+        if self.overlap:
+            _lib.check(self._fn(*self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
+                       "run_frames_overlap")
+        else:
+            _lib.check(self._fn(*self._args(), dv.stream()), "run_frames")
 
     def capture(self):
         """Record one launch into a CUDA graph (static shapes and buffers)."""
@@ -199,15 +168,38 @@ class FramePipeline:
         self.graph.replay()
 
     # -- outputs ------------------------------------------------------------
-    def results(self, est: bool = True) -> dict:
+    def check_status(self, status=None):
+        """Raise if any (frame, user) trainer reported a failure in its status
+        word: DegenerateSampleError (apsm.py:325-328) or a RuntimeError when
+        the trainer's pipeline watchdog cut the chain short."""
+        st = self.status.cpu().numpy() if status is None else np.asarray(status)
+        raise_for_status(st)
+
+    def results(self, est: bool = True, check: bool = True) -> dict:
         out = dict(labels=self.labels.cpu().numpy(), bit_err=self.bit_err.cpu().numpy(),
                    sym_err=self.sym_err.cpu().numpy(), n_active=self.n_active.cpu().numpy(),
                    status=self.status.cpu().numpy(), theta=self.theta.cpu().numpy(),
                    coeff=self.coeff.cpu().numpy(), first_step=self.first_step.cpu().numpy())
+        if check:
+            self.check_status(out["status"])
         if est and self.est is not None:
             e = self.est.cpu().numpy().astype(np.float64)
             out["est"] = e[..., 0] + 1j * e[..., 1]
         return out
+
+
+def raise_for_status(status):
+    """Trainer status words (F x K int32) -> the reference's exceptions."""
+    st = np.asarray(status)
+    if np.any(st & _lib.TRAIN_DEGENERATE):
+        from .apsm import DegenerateSampleError
+        raise DegenerateSampleError(
+            "kappa(r, r) = 0: zero sample vector with a weightless Gaussian kernel")
+    if np.any(st & _lib.TRAIN_STALLED):
+        raise RuntimeError("kapsm trainer pipeline watchdog fired: training was cut short "
+                           f"for (frame, user) {np.argwhere(st & _lib.TRAIN_STALLED).tolist()}")
+    if np.any(st):
+        raise RuntimeError(f"kapsm trainer status {sorted(set(st.ravel().tolist()))}")
 
 
 def _event_handle(ev) -> int:
@@ -254,6 +246,7 @@ class FrameStream:
         pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         self.labels_h = [pin(p.labels) for p in self.pipes]
         self.counts_h = [pin(torch.stack([p.bit_err, p.sym_err])) for p in self.pipes]
+        self.status_h = [pin(p.status) for p in self.pipes]
         ev = lambda: [torch.cuda.Event() for _ in range(depth)]
         self.ev_in, self.ev_comp, self.ev_out = ev(), ev(), ev()
         self.used = [False] * depth
@@ -264,7 +257,7 @@ class FrameStream:
         self.ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(depth)]
         lib = _lib.load()
         self._fin, self._fout = lib.kapsm_stream_frame_in, lib.kapsm_stream_frame_out
-        VP, UL = C.c_void_p * 3, C.c_ulonglong * 3
+        VP, UL, VP4, UL4 = C.c_void_p * 3, C.c_ulonglong * 3, C.c_void_p * 4, C.c_ulonglong * 4
         self._slot = []
         for k, p in enumerate(self.pipes):
             # with no collectives the slot's "inputs free" point is the graph's end
@@ -273,10 +266,12 @@ class FrameStream:
                 "dst_in": VP(p.rx.data_ptr(), p.pilots.data_ptr(), p.tx.data_ptr()),
                 "bytes_in": UL(*(t.numel() * t.element_size() for t in (p.rx, p.pilots, p.tx))),
                 "src_in": VP(0, 0, 0),
-                "dst_out": VP(self.labels_h[k].data_ptr(), self.counts_h[k][0].data_ptr(),
-                              self.counts_h[k][1].data_ptr()),
-                "src_out": VP(p.labels.data_ptr(), p.bit_err.data_ptr(), p.sym_err.data_ptr()),
-                "bytes_out": UL(p.labels.numel(), p.bit_err.numel() * 8, p.sym_err.numel() * 8),
+                "dst_out": VP4(self.labels_h[k].data_ptr(), self.counts_h[k][0].data_ptr(),
+                               self.counts_h[k][1].data_ptr(), self.status_h[k].data_ptr()),
+                "src_out": VP4(p.labels.data_ptr(), p.bit_err.data_ptr(), p.sym_err.data_ptr(),
+                               p.status.data_ptr()),
+                "bytes_out": UL4(p.labels.numel(), p.bit_err.numel() * 8, p.sym_err.numel() * 8,
+                                 p.status.numel() * 4),
                 "graph": p.graph.raw_cuda_graph_exec(),
                 "ev_in": _event_handle(self.ev_in[k]), "ev_comp": _event_handle(comp_ev),
                 "ev_out": _event_handle(self.ev_out[k]), "ev_end": _event_handle(self.ev_end[k]),
@@ -323,7 +318,7 @@ class FrameStream:
             ready = sl["ev_comp"]
         else:
             ready = sl["ev_end"]
-        _lib.check(self._fout(self.d2h.cuda_stream, ready, 3, sl["dst_out"], sl["src_out"],
+        _lib.check(self._fout(self.d2h.cuda_stream, ready, 4, sl["dst_out"], sl["src_out"],
                               sl["bytes_out"], sl["ev_out"]), "stream_frame_out")
         self.used[slot] = True
         self.n += 1
@@ -346,6 +341,7 @@ class FrameStream:
             raise ValueError(f"ticket {ticket} is no longer (or not yet) held")
         slot = ticket % self.depth
         self.ev_out[slot].synchronize()
+        raise_for_status(self.status_h[slot].numpy())
         return self.labels_h[slot], self.counts_h[slot][0], self.counts_h[slot][1]
 
 

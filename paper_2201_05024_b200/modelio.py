@@ -53,14 +53,18 @@ class _Reader:
         raise FileFormatError(f"{self.path}: {msg}")
 
     def header(self, dtype: np.dtype, magic: bytes):
+        """Magic first (offset 0), then the rest of the header as one read at
+        offset 8, so a short file names the field that is cut (modelio.py:53-72)."""
         n = len(self.buf)
-        if n < len(magic) or self.buf[:len(magic)] != magic:
-            got = self.buf[:len(magic)]
-            self.fail(f"bad {self.kind} magic at offset 0: {got!r} (expected {magic!r})"
-                      if n >= len(magic) else
-                      f"truncated {self.kind} file: {n} bytes, the magic needs {len(magic)} "
+        if n < len(magic):
+            self.fail(f"truncated {self.kind} file: {n} bytes, header needs {len(magic)} "
                       f"at offset 0")
-        return self.array(dtype, 1, f"{self.kind} header")[0]
+        if self.buf[:len(magic)] != magic:
+            self.fail(f"bad {self.kind} magic at offset 0: {self.buf[:len(magic)]!r} != {magic!r}")
+        self.pos = len(magic)
+        rest = np.dtype([(k, dtype.fields[k][0]) for k in dtype.names if k != "magic"])
+        self.array(rest, 1, f"{self.kind} header")
+        return np.frombuffer(self.buf, dtype=dtype, count=1, offset=0)[0]
 
     def array(self, dtype, count: int, what: str):
         dtype = np.dtype(dtype)
@@ -151,7 +155,7 @@ def load_symbols(path) -> np.ndarray:
     """Raw float32 (I, Q) stream -> complex128."""
     size = os.path.getsize(path)
     if size % 8:
-        raise FileFormatError(f"{path}: symbol stream of {size} bytes is not whole (I, Q) "
-                              f"float32 pairs (partial pair at offset {size - size % 8})")
+        raise FileFormatError(f"{path}: symbol stream length {size} is not a multiple of 8 "
+                              f"(truncated pair at offset {size - size % 8})")
     v = np.fromfile(path, dtype="<f4").astype(np.float64).reshape(-1, 2)
     return v[:, 0] + 1j * v[:, 1]

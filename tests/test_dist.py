@@ -37,6 +37,10 @@ def _worker(rank, world, port, q):
             lab = torch.full((1, K, nd), 10 * rank + fi, dtype=torch.uint8)
             steps += ex.add(lab, torch.tensor([1, rank], dtype=torch.int64))
         bx = (steps, tuple(ex.gathered.shape), ex.gathered[:, :, 0, 0].tolist(), ex.totals.tolist())
+        # the trailing partial batch (frame 4 of each rank) is exchanged by flush()
+        fl = ex.flush()
+        bx += (fl, tuple(ex.gathered.shape), ex.gathered[:, :, 0, 0].tolist(), ex.totals.tolist(),
+               ex.flush(), ex.pending)
         q.put((rank, frames, tuple(g.shape), g[:, 0, 0, 0].tolist(), counts.tolist(), bx))
       except Exception as e:  # report instead of hanging the parent
         q.put((rank, "error", repr(e), None, None, None))
@@ -71,4 +75,5 @@ def test_gather_and_reduce_world2_gloo():
     assert v0 == [1, 2] and v1 == [1, 2]
     assert c0 == c1 == [[1, 10, 2]]
     # last exchanged batch = frames 2, 3 of each rank; counters summed over 2 frames x 2 ranks
-    assert b0 == b1 == (2, (2, 2, 3, 5), [[2, 3], [12, 13]], [4, 2])
+    assert b0 == b1 == (2, (2, 2, 3, 5), [[2, 3], [12, 13]], [4, 2],
+                        True, (2, 1, 3, 5), [[4], [14]], [2, 1], False, 0)

@@ -1,0 +1,150 @@
+"""GPU parity at every BASELINE.json config and at the reference's frozen
+acceptance results, against fixtures written by the unmodified reference
+(tests/golden/make_golden_r2.py):
+
+* C1 (K=6, M=16, QPSK, 685/3840) on seeds 0..19, all 6 users, FP32 and FP64
+  frame pipelines: decisions (every payload symbol) and bit / symbol error
+  counts identical, atom counts identical, soft estimates within 1e-4 (FP32)
+  / 1e-9 (FP64) relative (max-norm over the frame);
+* C4 (K=16, M=64, 16-QAM, 685/3840) seed 0, all 16 users, the same bars;
+  users 0-3 also with the trained filters (FP64: atoms identical in slot
+  order, theta / coefficients within 1e-9) and the full soft estimates;
+* ``run_trial`` driven exactly as pkg/tests/test_acceptance.py:63-75 drives
+  it (criteria 5/6/7, 20 seeds per cell): per-seed BER and trained_atoms
+  identical to the reference with the float64 and the float32 engine, and
+  the frozen means of pkg/test_output.txt:246-248.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2201_05024_b200 as K
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"f32": 1e-4, "f64": 1e-9}
+
+
+def maxrel(a, b, d=None):
+    d = np.max(np.abs(b)) if d is None else d
+    return float(np.max(np.abs(a - b)) / d)
+
+
+def _check_table(g, seeds, Kn, M, scheme, prec, F):
+    """FramePipeline over F frames at a time against a per-(seed, user) table."""
+    sub = int(g["sub"])
+    for s0 in range(0, len(seeds), F):
+        ss = seeds[s0:s0 + F]
+        rx, pil, tx, _ = K.host_frames(ss, Kn, M, 685, 3840, scheme)
+        pipe = K.FramePipeline(len(ss), Kn, M, 685, 3840, scheme, precision=prec)
+        pipe.load(rx, pil, tx)
+        pipe.launch()
+        r = pipe.results()
+        for i, s in enumerate(ss):
+            row = list(g["seeds"]).index(s)
+            assert np.array_equal(r["labels"][i], g["labels"][row]), (s, prec)
+            assert np.array_equal(r["bit_err"][i], g["bit_err"][row]), (s, prec)
+            assert np.array_equal(r["sym_err"][i], g["sym_err"][row]), (s, prec)
+            assert np.array_equal(r["n_active"][i], g["n_atoms"][row]), (s, prec)
+            for u in range(Kn):
+                dev = maxrel(r["est"][i, u, ::sub], g["est_sub"][row, u], g["est_max"][row, u])
+                assert dev < TOL[prec], (s, u, prec, dev)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_c1_twenty_seeds_all_users(prec):
+    g = np.load(os.path.join(GOLDEN, "c1_seeds20.npz"))
+    _check_table(g, list(range(20)), 6, 16, "QPSK", prec, F=10)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_c1_single_frame_latency_pipeline(prec):
+    """The latency configuration (one frame per launch, graph replay) on
+    seeds 0..3: the same decisions as the reference."""
+    g = np.load(os.path.join(GOLDEN, "c1_seeds20.npz"))
+    for s in range(4):
+        rx, pil, tx, _ = K.host_frames([s], 6, 16, 685, 3840, "QPSK")
+        pipe = K.FramePipeline(1, 6, 16, 685, 3840, "QPSK", precision=prec)
+        pipe.load(rx, pil, tx)
+        pipe.capture()
+        pipe.replay()
+        r = pipe.results()
+        assert np.array_equal(r["labels"][0], g["labels"][s])
+        assert np.array_equal(r["bit_err"][0], g["bit_err"][s])
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_c4_all_users(prec):
+    g = np.load(os.path.join(GOLDEN, "c4_s0_all_users.npz"))
+    _check_table(g, [0], 16, 64, "QAM16", prec, F=1)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_c4_users0123_full_estimates(prec):
+    g = np.load(os.path.join(GOLDEN, "c4_s0_users0123.npz"))
+    rx, pil, tx, _ = K.host_frames([0], 16, 64, 685, 3840, "QAM16")
+    assert np.array_equal(rx[0, :4], g["rx_head"])
+    pipe = K.FramePipeline(1, 16, 64, 685, 3840, "QAM16", precision=prec)
+    pipe.load(rx, pil, tx)
+    pipe.launch()
+    r = pipe.results()
+    for u in range(4):
+        assert maxrel(r["est"][0, u], g[f"u{u}_est"]) < TOL[prec]
+        assert int(r["bit_err"][0, u]) == int(g[f"u{u}_bit_err"])
+        assert int(r["n_active"][0, u]) == int(g[f"u{u}_n_atoms"])
+
+
+def test_c4_trained_filters_f64():
+    """K.train (FP64) on C4 pilots: identical atoms in the reference's slot
+    order, theta and coefficients within 1e-9."""
+    g = np.load(os.path.join(GOLDEN, "c4_s0_users0123.npz"))
+    fr = K.seeded_frame(0, 16, 64, 685, 3840, "QAM16")
+    R = K.realify_batch(fr["rx"][:685])
+    for u in range(4):
+        f = K.train(None, zip(fr["rx"][:685], fr["symbols"][u, :685]), K.ApsmConfig(),
+                    precision="f64")
+        assert f.n_atoms == int(g[f"u{u}_n_atoms"])
+        assert np.array_equal(f.atoms, R[g[f"u{u}_atom_idx"]])
+        np.testing.assert_allclose(f.theta, g[f"u{u}_theta"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(f.coeffs, g[f"u{u}_coeffs"], rtol=1e-8, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- run_trial
+_PARAMS = {"partial": K.KernelParams(0.5, 0.5, 0.05), "linear": K.KernelParams(1.0, 0.0, 0.05)}
+
+
+def _trials(engine):
+    g = np.load(os.path.join(GOLDEN, "trial_anchors.npz"))
+    out = {}
+    for c, cell in enumerate(g["cells"]):
+        scheme, si, m, pname = str(cell).split("|")
+        si, m = int(si), int(m)
+        bers, atoms = [], []
+        for seed in range(20):
+            rng = np.random.default_rng([seed, si, m])
+            ch = K.draw_channel(6, m, "uniform", 0.06, rng)
+            rep = K.run_trial(ch, K.FrameSpec(685, 3840, scheme),
+                              K.ApsmConfig(params=_PARAMS[pname]), engine, 0, rng)
+            bers.append(rep.ber)
+            atoms.append(rep.trained_atoms)
+        out[str(cell)] = (np.array(bers), np.array(atoms), c)
+    return g, out
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_run_trial_acceptance_anchors(prec):
+    g, res = _trials(K.EngineConfig(precision=prec))
+    ref = g["ber_f64"] if prec == "f64" else g["ber_f32"]
+    for cell, (bers, atoms, c) in res.items():
+        assert np.array_equal(bers, ref[c]), (cell, bers, ref[c])
+        assert np.array_equal(atoms, g["trained_atoms"][c]), cell
+    mean = {cell: float(v[0].mean()) for cell, v in res.items()}
+    # pkg/test_output.txt:246-248 (criteria 5, 6, 7)
+    assert mean["BPSK|0|16|partial"] == 0.0 and mean["QPSK|1|16|partial"] == 0.0
+    assert f"{mean['QAM16|2|16|partial']:.2e}" == "3.26e-06"
+    assert f"{mean['QPSK|1|4|partial']:.2e}" == "1.74e-01"
+    assert mean["QPSK|1|8|partial"] == mean["QPSK|1|12|partial"] == 0.0
+    assert f"{mean['QPSK|1|3|partial']:.4f}" == "0.2058"
+    assert f"{mean['QPSK|1|3|linear']:.4f}" == "0.2133"

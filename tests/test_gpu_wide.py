@@ -2,7 +2,8 @@
 latency kernel's W <= 23 and pilot counts beyond Np = 3072 -- BASELINE.json's
 C3 dictionary/window sweep and the C4 full-band frame -- against the CPU
 oracle (oracle/kapsm_oracle.py, pinned to the reference's golden vectors).
-KAPSM_FORCE_WIDE routes the small golden cases through the same kernel."""
+The ``force_wide`` fixture routes the small golden cases through the same
+kernel (its C-ABI entry kapsm_train_general_*)."""
 
 import glob
 import os
@@ -26,7 +27,7 @@ def maxrel(a, b):
 
 @pytest.fixture
 def force_wide(monkeypatch):
-    monkeypatch.setenv("KAPSM_FORCE_WIDE", "1")
+    monkeypatch.setattr(K.apsm, "_TRAIN_ENTRY", "kapsm_train_general")
 
 
 def _check(f, ref, tol=1e-8):
@@ -73,7 +74,7 @@ def test_wide_generic_stream_and_warm_start(force_wide):
     s = t2.state()
     assert np.array_equal(s.atoms[:2], f0.atoms) and np.array_equal(s.coeffs[:2], f0.coeffs)
     # the same state from the oracle-checked default path (latency kernel)
-    os.environ.pop("KAPSM_FORCE_WIDE")
+    K.apsm._TRAIN_ENTRY = "kapsm_train"
     t3 = K.ApsmTrainer(4, cfg, f0=f0)
     for r, b in zip(R[:40], B[:40]):
         t3.observe(r, b)

@@ -91,3 +91,46 @@ def test_reference_known_answers():
     assert m["coeff"][0] == 0.0 and m["n_atoms"] == 0
     m = O.train_user(np.array([[1.0, 0.0]]), np.array([-1.0]), W=1, eps=0.1)
     assert abs(m["coeff"][0] + 0.9) < 1e-15
+
+
+def test_c1_seed_table_spot_checks():
+    """The oracle reproduces the reference's C1 seed table (c1_seeds20.npz,
+    tests/golden/make_golden_r2.py) on two (seed, user) pairs."""
+    g = np.load(os.path.join(GOLDEN, "c1_seeds20.npz"))
+    sub = int(g["sub"])
+    for seed, u in ((7, 3), (19, 5)):
+        fr = O.make_frame(seed, 6, 16, 685, 3840, "QPSK")
+        r = O.run_frame(fr, 685, "QPSK", users=[u])[0]
+        assert r["model"]["n_atoms"] == int(g["n_atoms"][seed, u])
+        assert r["bit_err"] == int(g["bit_err"][seed, u])
+        assert r["sym_err"] == int(g["sym_err"][seed, u])
+        assert np.array_equal(r["rx_idx"], g["labels"][seed, u])
+        dev = np.max(np.abs(r["est"][::sub] - g["est_sub"][seed, u])) / g["est_max"][seed, u]
+        assert dev < 1e-6                      # fixture stored as complex64
+
+
+def test_c4_massive_frame_user0():
+    """C4 (K=16, M=64, 16-QAM): the oracle reproduces the reference's user-0
+    filter (slot order) and soft estimates."""
+    g = np.load(os.path.join(GOLDEN, "c4_s0_users0123.npz"))
+    fr = O.make_frame(0, 16, 64, 685, 3840, "QAM16")
+    assert np.array_equal(fr["rx"][:4], g["rx_head"])
+    r = O.run_frame(fr, 685, "QAM16", users=[0])[0]
+    assert r["model"]["n_atoms"] == int(g["u0_n_atoms"])
+    assert np.array_equal(r["model"]["slot_index"], g["u0_atom_idx"])
+    np.testing.assert_allclose(r["model"]["theta"], g["u0_theta"], rtol=1e-11, atol=1e-13)
+    assert np.max(np.abs(r["est"] - g["u0_est"])) <= 1e-11 * np.max(np.abs(g["u0_est"]))
+    assert r["bit_err"] == int(g["u0_bit_err"])
+
+
+def test_trial_anchor_means_match_frozen_log():
+    """trial_anchors.npz (reference run_trial, 20 seeds per cell) reproduces
+    the frozen acceptance means of pkg/test_output.txt:246-248, and the
+    float32 engine gives the same per-seed BER as the float64 one."""
+    g = np.load(os.path.join(GOLDEN, "trial_anchors.npz"))
+    m = dict(zip([str(c) for c in g["cells"]], g["ber_f64"].mean(1)))
+    assert m["BPSK|0|16|partial"] == 0 and m["QPSK|1|16|partial"] == 0
+    assert f"{m['QAM16|2|16|partial']:.2e}" == "3.26e-06"
+    assert f"{m['QPSK|1|4|partial']:.2e}" == "1.74e-01"
+    assert f"{m['QPSK|1|3|partial']:.4f}" == "0.2058" and f"{m['QPSK|1|3|linear']:.4f}" == "0.2133"
+    assert np.array_equal(g["ber_f64"], g["ber_f32"])
