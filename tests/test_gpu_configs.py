@@ -50,7 +50,9 @@ def _check_table(g, seeds, Kn, M, scheme, prec, F):
             assert np.array_equal(r["n_active"][i], g["n_atoms"][row]), (s, prec)
             for u in range(Kn):
                 dev = maxrel(r["est"][i, u, ::sub], g["est_sub"][row, u], g["est_max"][row, u])
-                assert dev < TOL[prec], (s, u, prec, dev)
+                # the table stores complex64 estimates (~6e-8 relative): FP64's
+                # 1e-9 bar is checked on the full-precision fixtures below
+                assert dev < max(TOL[prec], 1e-6), (s, u, prec, dev)
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
