@@ -213,7 +213,9 @@ def _event_handle(ev) -> int:
 
 class FrameStream:
     """Streaming frames from pinned host memory with copy/compute overlap
-    (pinned, double-buffered H2D).
+    (pinned, double-buffered H2D).  Each submission is one
+    frame, or a batch of ``frames`` frames (throughput mode, one captured
+    multi-frame pipeline per slot).
 
     ``depth`` FramePipelines (each captured into its own CUDA graph) are used
     round-robin.  Frame i's host->device copy runs on an H2D stream while frame
@@ -230,12 +232,15 @@ class FrameStream:
 
     def __init__(self, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32", depth: int = 2,
-                 device=None, post=None, concurrent: bool = False):
+                 device=None, post=None, concurrent: bool = False, frames: int = 1):
         if depth < 1:
             raise ValueError(f"depth must be >= 1, got {depth}")
+        if frames < 1:
+            raise ValueError(f"frames must be >= 1, got {frames}")
         dev = dv.device() if device is None else device
         self.depth = depth
-        self.pipes = [FramePipeline(1, K, M, n_train, n_data, scheme, cfg=cfg,
+        self.frames = frames
+        self.pipes = [FramePipeline(frames, K, M, n_train, n_data, scheme, cfg=cfg,
                                     precision=precision, store_est=False, device=dev)
                       for _ in range(depth)]
         for p in self.pipes:
@@ -280,8 +285,9 @@ class FrameStream:
         self.n = 0
 
     def submit(self, rx, pilots, tx_labels, start_event=None, timing=None) -> int:
-        """Queue one frame: tensors shaped like FramePipeline.load's inputs for
-        F = 1 (float32/float64 interleaved rx and pilots, uint8 labels), pinned
+        """Queue one batch of ``frames`` frames (one frame by default): tensors
+        shaped like FramePipeline.load's inputs for F = ``frames``
+        (float32/float64 interleaved rx and pilots, uint8 labels), pinned
         host or device-resident; they are copied into the slot's buffers on the
         copy stream and the slot's captured graph runs on its compute stream --
         one library call (``kapsm_stream_frame_in``), results come back with a
