@@ -391,11 +391,26 @@ int launch_finish(const T* rx, long long rx_stride, int F, int K, int n_train, i
   return status_from(cudaGetLastError());
 }
 
+int screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data, int M,
+              kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals, cudaStream_t s);
+
 template <typename T>
 int screen(const T* rx, long long rx_stride, int F, int n_train, int n_data, int M,
-           kapsm_kernel_params p, unsigned* live, cudaStream_t s) {
+           kapsm_kernel_params p, unsigned* live, cudaStream_t s, bool tensor_cores = true) {
   if (F < 0 || n_train < 0 || n_data < 0 || M < 1 || !rx || !live) return KAPSM_ERR_INVALID;
   if (F == 0 || n_data == 0 || n_train == 0) return KAPSM_OK;
+  if constexpr (sizeof(T) == 4) {
+    // FP32: the tensor-core screen (screen_tc.cu) up to M = 64; FP64 (the
+    // parity precision) keeps the SIMT screen with the FP64 threshold
+    if (tensor_cores) {
+      char* ws = reinterpret_cast<char*>(live);
+      int* cnt = reinterpret_cast<int*>(ws + ws_live(F, n_train, n_data));
+      float4* vals = reinterpret_cast<float4*>(
+          ws + (ws_live(F, n_train, n_data) + ws_cnt(F, n_data) + 15) / 16 * 16);
+      const int r = screen_tc(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
+      if (r != KAPSM_ERR_UNSUPPORTED) return r;
+    }
+  }
   if (M <= 4) return launch_screen<T, 4>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
   if (M <= 8) return launch_screen<T, 8>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
   if (M <= 16) return launch_screen<T, 16>(rx, rx_stride, F, n_train, n_data, M, p, live, s);
@@ -436,6 +451,16 @@ int finish(const T* rx, long long rx_stride, int F, int K, int n_train, int n_da
   }
 KAPSM_SCREEN_ENTRY(kapsm_detect_screen_f32, float)
 KAPSM_SCREEN_ENTRY(kapsm_detect_screen_f64, double)
+
+// Internal (tests, not in the public header): the FP32 SIMT screen, the
+// reference point of the tensor-core classifier's superset property.
+extern "C" int kapsm_internal_screen_simt_f32(const float* rx, long long rx_stride, int F,
+                                              int n_train, int n_data, int M,
+                                              kapsm_kernel_params p, unsigned* live,
+                                              void* stream) {
+  return kapsm::screen<float>(rx, rx_stride, F, n_train, n_data, M, p, live,
+                              (cudaStream_t)stream, false);
+}
 
 #define KAPSM_FINISH_ENTRY(NAME, T)                                                             \
   extern "C" int NAME(const T* rx, long long rx_stride, int F, int K, int n_train, int n_data,  \

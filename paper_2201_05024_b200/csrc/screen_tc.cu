@@ -1,0 +1,351 @@
+// K3a on the 5th-generation tensor cores: the (pilot x payload) kernel screen
+// of the detection (engine.py:137-147 restated as a dead/live classifier, see
+// screen.cu) with its cross term x_p^H y_t computed by tcgen05.mma (TF32
+// operands from shared memory, FP32 accumulators in TMEM).
+//
+// Per payload symbol t and pilot p of a frame the three realified Gaussian
+// distances of the 2x2 kernel block are nx + ny - 2 Re c and nx + ny -+ 2 Im c,
+// c = x_p^H y_t; the block is dead when even the smallest one underflows the
+// FP32 exponential.  With realified rows in the rx layout (re, im interleaved
+// per antenna), Re c = x . y and Im c = x . rot(y), rot(y) = (im, -re) per
+// antenna, so one real GEMM A[pilots x 2M] . B[2 NT x 2M]^T gives both: B
+// holds NT payload rows and their NT rotated copies (MMA N = 2 NT).
+//
+// TF32 keeps 10 mantissa bits, so the cross term carries an error of at most
+// 2^-9 |x||y| <= 2^-10 (nx + ny) per component: a pair is declared live when
+//      nx + ny - 2 max(Re c, |Im c|) < T0 + (nx + ny) / 128,   T0 = dead / inv2s,
+// a margin of 4x that bound.  The classifier is therefore conservative (it can
+// only add live pairs), and every live pair is recomputed exactly with
+// explicit differences (kernels.py:187-191) -- here for the compact list, in
+// detect_finish otherwise -- so the detector's outputs do not depend on TF32.
+//
+// CTA = NT payload symbols of one frame x all pilots:
+//   * B (2 NT rows) and two M-tile buffers of A (128 pilots each) in shared
+//     memory, K-major with the 128-byte swizzle (1024-byte atoms of 8 rows),
+//     one atom column per 32 floats of the row (KC chunks);
+//   * thread 0 issues KC x 4 MMAs (M = 128, N = 2 NT, K = 8) per pilot tile and
+//     commits them to an mbarrier; the next tile's cp.async copies overlap;
+//   * 8 epilogue warps read the accumulators (tcgen05.ld 32x32b.x32: warp w
+//     reads TMEM lanes 32 (w % 4) .. +31 = 32 pilots, half of the columns),
+//     test each (pilot, symbol) pair and ballot the results into the live-bit
+//     words (bit = pilot, word per symbol) -- the word layout of screen.cu;
+//   * the live words and the compact per-symbol lists go out as in screen.cu.
+#include "kapsm_common.cuh"
+
+namespace kapsm {
+
+constexpr int TC_THREADS = 256;
+constexpr int TC_MROWS = 128;            // pilots per MMA tile (M)
+constexpr int TC_CAP = 8;                // == SC_CAP (screen.cu): list entries per symbol
+
+// ---- tcgen05 / descriptor helpers ----
+KAPSM_DEV unsigned long long umma_desc_sw128(unsigned saddr) {
+  // K-major, SWIZZLE_128B: start >> 4 (bits 0-13), LBO (unused) = 1, SBO = 1024 B
+  // between 8-row groups (bits 32-45), version 1 (bits 46-47), layout 2 (61-63)
+  const unsigned lo = ((saddr >> 4) & 0x3FFFu) | (1u << 16);
+  const unsigned hi = (1024u >> 4) | (1u << 14) | (2u << 29);
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+KAPSM_DEV void umma_tf32(unsigned tmem_d, unsigned long long a, unsigned long long b,
+                         unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+KAPSM_DEV void umma_commit(unsigned mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(mbar) : "memory");
+}
+
+KAPSM_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+KAPSM_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+KAPSM_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+KAPSM_DEV void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+KAPSM_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+KAPSM_DEV void sts_f4(unsigned a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// byte offset of 16-byte unit j (0..7) of row r inside a K chunk of 8-row
+// 1024-byte atoms (the SWIZZLE_128B pattern: unit index XOR row-in-atom)
+KAPSM_DEV unsigned sw128_off(int r, int j) {
+  return (unsigned)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+// float4 number q (4 q .. 4 q + 3) of a row of n = 2M floats, zero beyond n
+KAPSM_DEV float4 row_f4(const float* row, int q, int n, bool vec) {
+  const int e = 4 * q;
+  if (vec && e + 4 <= n) return __ldg(reinterpret_cast<const float4*>(row + e));
+  float4 v;
+  v.x = e < n ? row[e] : 0.f;
+  v.y = e + 1 < n ? row[e + 1] : 0.f;
+  v.z = e + 2 < n ? row[e + 2] : 0.f;
+  v.w = e + 3 < n ? row[e + 3] : 0.f;
+  return v;
+}
+
+template <int NT, int KC>
+struct TcSmem {
+  static constexpr int B_BYTES = 2 * NT * 128 * KC;
+  static constexpr int A_BYTES = TC_MROWS * 128 * KC;
+  static constexpr int OFF_B = 0;
+  static constexpr int OFF_A = B_BYTES;                  // two buffers
+  static constexpr int OFF_BITS = OFF_A + 2 * A_BYTES;
+  static size_t bytes(int NW) {
+    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 64;
+  }
+};
+
+template <int NT, int KC>
+__global__ void __launch_bounds__(TC_THREADS)
+    detect_screen_tc_kernel(const float* __restrict__ rx, long long rx_stride, int n_train,
+                            int n_data, int M, float inv2s, float dead,
+                            unsigned* __restrict__ live, int* __restrict__ cnt,
+                            float4* __restrict__ vals) {
+  using L = TcSmem<NT, KC>;
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte aligned base for the swizzle atoms
+  const unsigned raw_s = smem_u32(smem_raw);
+  const unsigned base_s = (raw_s + 1023u) & ~1023u;
+  unsigned char* base = smem_raw + (base_s - raw_s);
+  const int NW = (n_train + 31) / 32;
+  unsigned* bits = reinterpret_cast<unsigned*>(base + L::OFF_BITS);        // [NW][NT]
+  float* nyb = reinterpret_cast<float*>(base + L::OFF_BITS + (size_t)NW * NT * 4);
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nyb + NT);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(mbar + 1);
+  const unsigned sB = base_s + L::OFF_B, sA = base_s + L::OFF_A;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int f = blockIdx.y, t0 = blockIdx.x * NT;
+  const int D = 2 * M;
+  const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
+  const float* Xf = rx + (long long)f * rx_stride;
+  const float* Yf = Xf + (long long)n_train * D;
+  const int n_mt = (n_train + TC_MROWS - 1) / TC_MROWS;
+
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(2 * NT) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+
+  // ---- B: NT payload rows (Re) and their rotations (Im), zero past n_data ----
+  for (int e = tid; e < NT * KC * 8; e += TC_THREADS) {
+    const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
+    const int t = t0 + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < n_data) v = row_f4(Yf + (long long)t * D, kc * 8 + j, D, vec);
+    const unsigned chunk = (unsigned)kc * (2 * NT) * 128;
+    sts_f4(sB + chunk + sw128_off(r, j), v);
+    sts_f4(sB + chunk + sw128_off(NT + r, j), make_float4(v.y, -v.x, v.w, -v.z));
+  }
+
+  // ---- A tile loader: pilots p0 .. p0 + 127 into buffer b ----
+  auto load_a = [&](int mt, int b) {
+    const int p0 = mt * TC_MROWS;
+    const unsigned sa = sA + (unsigned)b * L::A_BYTES;
+    for (int e = tid; e < TC_MROWS * KC * 8; e += TC_THREADS) {
+      const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
+      const int p = p0 + r;
+      const unsigned d = sa + (unsigned)kc * TC_MROWS * 128 + sw128_off(r, j);
+      const float* src = Xf + (long long)p * D + 4 * (kc * 8 + j);
+      if (p < n_train && vec && 4 * (kc * 8 + j) + 4 <= D) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+      } else {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p < n_train) v = row_f4(Xf + (long long)p * D, kc * 8 + j, D, vec);
+        sts_f4(d, v);
+      }
+    }
+    cp_async_commit();
+  };
+  load_a(0, 0);
+
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = *tmem_slot;
+  // symbol norms (scaled half, see the live test below)
+  const float shrink = 0.5f * (1.0f - 1.0f / 128.0f);
+  for (int r = tid; r < NT; r += TC_THREADS) {
+    float s = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = lds_f4(sB + (unsigned)kc * (2 * NT) * 128 + sw128_off(r, j));
+        s = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s))));
+      }
+    nyb[r] = shrink * s;
+  }
+
+  // instruction descriptor: F32 accumulate, TF32 A and B, both K-major,
+  // N = 2 NT (bits 17-22, >> 3), M = 128 (bits 24-28, >> 4)
+  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(2 * NT >> 3) << 17) |
+                         ((unsigned)(TC_MROWS >> 4) << 24);
+  const float half_t0 = 0.5f * dead / inv2s;
+  const int q = warp & 3;                   // TMEM lane quarter = pilots 32q .. 32q + 31
+  constexpr int CH = NT / 64;               // 32-symbol column chunks per warp
+  const int col0 = (warp >> 2) * (NT / 2);
+
+  for (int mt = 0; mt < n_mt; ++mt) {
+    cp_async_wait<0>();
+    fence_async_smem();
+    __syncthreads();                        // A[mt] visible; previous epilogue done with TMEM
+    if (tid == 0) {
+      tc_fence_after();
+      const unsigned sa = sA + (unsigned)(mt & 1) * L::A_BYTES;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const unsigned long long a = umma_desc_sw128(sa + kc * TC_MROWS * 128 + ks * 32);
+          const unsigned long long b = umma_desc_sw128(sB + kc * (2 * NT) * 128 + ks * 32);
+          umma_tf32(tmem, a, b, idesc, (kc | ks) ? 1u : 0u);
+        }
+      umma_commit(smem_u32(mbar));
+    }
+    if (mt + 1 < n_mt) load_a(mt + 1, (mt + 1) & 1);
+
+    // this lane's pilot norm (row 32q + lane of the tile) while the MMAs run
+    const int prow = 32 * q + lane, p = mt * TC_MROWS + prow;
+    float a_thr;
+    {
+      const unsigned sa = sA + (unsigned)(mt & 1) * L::A_BYTES;
+      float s = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = lds_f4(sa + (unsigned)kc * TC_MROWS * 128 + sw128_off(prow, j));
+          s = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s))));
+        }
+      // live <=> max(Re c, |Im c|) > shrink (nx + ny) - T0 / 2
+      a_thr = p < n_train ? fmaf(shrink, s, -half_t0) : __int_as_float(0x7f800000);
+    }
+    while (!mbar_try_wait(mbar, (unsigned)(mt & 1))) {
+    }
+    tc_fence_after();
+    const int wrd = mt * (TC_MROWS / 32) + q;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int cb = col0 + 32 * c;
+      unsigned re[32], im[32];
+      const unsigned lane_sel = (unsigned)(32 * q) << 16;
+      tmem_ld32(tmem + lane_sel + (unsigned)cb, re);
+      tmem_ld32(tmem + lane_sel + (unsigned)(NT + cb), im);
+      tmem_wait_ld();
+      unsigned mine = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
+        const unsigned bj = __ballot_sync(0xffffffffu, m > a_thr + nyb[cb + j]);
+        mine = lane == j ? bj : mine;
+      }
+      if (wrd < NW) bits[wrd * NT + cb + lane] = mine;
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NT)
+                 : "memory");
+
+  // ---- live words out (word-major, coalesced over the symbols) ----
+  unsigned* lf = live + (long long)f * NW * n_data;
+  for (int i = tid; i < NW * NT; i += TC_THREADS) {
+    const int w = i / NT, tt = t0 + (i - w * NT);
+    if (tt < n_data) lf[(long long)w * n_data + tt] = bits[i];
+  }
+  // ---- compact list of each symbol's live pilots in pilot order, kernel
+  //      values from explicit differences (kernels.py:187-191); more than
+  //      TC_CAP: count -1, the finish recomputes from the words ----
+  for (int r = tid; r < NT; r += TC_THREADS) {
+    const int t = t0 + r;
+    if (t >= n_data) continue;
+    const float* y = Yf + (long long)t * D;
+    float4* vt = vals + ((long long)f * n_data + t) * TC_CAP;
+    int j = 0;
+    for (int w = 0; w < NW; ++w) {
+      unsigned b = bits[w * NT + r];
+      while (b) {
+        const int pp = w * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        if (j < TC_CAP) {
+          const float* x = Xf + (long long)pp * D;
+          float ea = 0.f, eb = 0.f, ec = 0.f;
+          for (int k = 0; k < M; ++k) {
+            const float xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+            float a0 = xr - yr, a1 = xi - yi;
+            ea = fmaf(a0, a0, fmaf(a1, a1, ea));
+            a0 = xr - yi; a1 = xi + yr;
+            eb = fmaf(a0, a0, fmaf(a1, a1, eb));
+            a0 = xr + yi; a1 = xi - yr;
+            ec = fmaf(a0, a0, fmaf(a1, a1, ec));
+          }
+          vt[j] = make_float4(exp_fast(-ea * inv2s), exp_fast(-eb * inv2s), exp_fast(-ec * inv2s),
+                              __int_as_float(pp));
+        }
+        ++j;
+      }
+    }
+    cnt[(long long)f * n_data + t] = j <= TC_CAP ? j : -1;
+  }
+}
+
+template <int NT, int KC>
+static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data,
+                            int M, kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals,
+                            cudaStream_t s) {
+  const int NW = (n_train + 31) / 32;
+  size_t smem = TcSmem<NT, KC>::bytes(NW);
+  // at least 112 KB: never co-resident with a latency-mode trainer CTA (120 KB),
+  // so the concurrent screen does not slow a critical warp down (screen.cu)
+  if (smem < 112 * 1024) smem = 112 * 1024;
+  if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
+  auto kern = detect_screen_tc_kernel<NT, KC>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return KAPSM_ERR_CUDA;
+  dim3 grid((n_data + NT - 1) / NT, F);
+  kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, M,
+                                      (float)(1.0 / (2.0 * p.sigma_sq)), 88.0f, live, cnt, vals);
+  return status_from(cudaGetLastError());
+}
+
+// the tensor-core screen for M <= 64 (2M <= 128 floats per row); returns
+// KAPSM_ERR_UNSUPPORTED beyond (the caller keeps the SIMT screen)
+int screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data, int M,
+              kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals, cudaStream_t s) {
+  if (M <= 16) return launch_screen_tc<128, 1>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
+  if (M <= 32) return launch_screen_tc<128, 2>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
+  if (M <= 64) return launch_screen_tc<64, 4>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
+  return KAPSM_ERR_UNSUPPORTED;
+}
+
+}  // namespace kapsm
