@@ -21,8 +21,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libkapsm_b200.so")
-SOURCES = ("gram.cu", "train.cu", "train_wide.cu", "detect.cu", "screen.cu", "screen_tc.cu",
-           "pipeline.cu")
+SOURCES = ("gram.cu", "train.cu", "train_wide.cu", "train_tp.cu", "detect.cu", "screen.cu",
+           "screen_tc.cu", "pipeline.cu")
 HEADERS = ("kapsm_common.cuh",)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -5,6 +5,48 @@
 // (noma.py:249-281) for every target user of each frame.
 #include "kapsm_common.cuh"
 
+namespace kapsm {
+bool train_tp_supported(int n_train, int M, int W);
+size_t train_tp_ws_bytes(int F, int n_train);
+int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
+             int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
+             void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
+             cudaStream_t s);
+}  // namespace kapsm
+
+static int pipe_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+// Throughput mode (more chains than SMs): the one-warp-per-chain trainer
+// (train_tp.cu) replaces K1 + K2 in FP32 when its limits hold (W <= 25,
+// M <= 64) and its workspace (band rows + pilot screen) fits in the caller's
+// Gram workspace.  Latency mode keeps the Gram-based trainer, whose critical
+// warp is the shorter per-step chain when a chain has SMs to itself.
+// trainer choice: AUTO as above, or forced (internal entry points: tests, A/B)
+enum TrainerMode { TRAINER_AUTO = 0, TRAINER_GRAM = 1, TRAINER_TP = 2 };
+
+template <typename T>
+static bool use_tp(int F, int K, int n_train, int M, int window, long long ld,
+                   int mode = TRAINER_AUTO) {
+  if constexpr (sizeof(T) != 4) {
+    return false;
+  } else {
+    if (mode == TRAINER_GRAM) return false;
+    const size_t cap = ((size_t)F * 2 * n_train + 32) * (size_t)ld * sizeof(T);
+    const bool fits = kapsm::train_tp_supported(n_train, M, window) &&
+                      kapsm::train_tp_ws_bytes(F, n_train) <= cap;
+    return fits && (mode == TRAINER_TP || (long long)F * K > pipe_num_sms());
+  }
+}
+
 template <typename T> struct Fns;
 template <> struct Fns<float> {
   static constexpr auto gram = kapsm_pilot_gram_f32;
@@ -37,8 +79,18 @@ static int run_frames(const T* rx, long long rx_stride, const T* pilots,
     return KAPSM_ERR_CUDA;
   if (sym_err && cudaMemsetAsync(sym_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess)
     return KAPSM_ERR_CUDA;
+  int r;
+  if constexpr (sizeof(T) == 4) {
+    if (use_tp<T>(F, K, n_train, M, window, ld)) {
+      r = kapsm::train_tp(rx, rx_stride, pilots, F, K, n_train, M, window, eps, p, qtab, gram_ws,
+                          coeff, first_step, theta, n_active, status, s);
+      if (r) return r;
+      return Fns<T>::detect(rx, rx_stride, F, K, n_train, n_data, M, coeff, theta, p, points,
+                            n_points, bps, tx_labels, est, labels, bit_err, sym_err, stream);
+    }
+  }
   const long long gstride = (long long)Np * ld;
-  int r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream);
+  r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream);
   if (r) return r;
   r = Fns<T>::train(gram_ws, ld, gstride, rx, rx_stride, nullptr, 0, 2 * M, pilots, F, K, Np,
                     window, eps, p, qtab, nullptr, nullptr, coeff, first_step, theta, n_active,
@@ -67,7 +119,7 @@ KAPSM_RUN_ENTRY(kapsm_run_frames_f64, double)
 // filters) on a side stream while K2 runs on the main stream; K3b finishes
 // once both are done.  Stream-ordered fork/join through events, so it captures into one
 // CUDA graph.
-template <typename T>
+template <typename T, int MODE = TRAINER_AUTO>
 static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
                               const unsigned char* tx_labels, int F, int K, int n_train,
                               int n_data, int M, int window, double eps, kapsm_kernel_params p,
@@ -89,6 +141,25 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
   }
   int r = KAPSM_OK;
   do {
+    if constexpr (sizeof(T) == 4) {
+      if (use_tp<T>(F, K, n_train, M, window, ld, MODE)) {
+        // detection screen forked at once (the band kernel is short); the
+        // one-warp-per-chain trainer on the main stream
+        if (cudaEventRecord(fork, s) != cudaSuccess ||
+            cudaStreamWaitEvent(s2, fork, 0) != cudaSuccess) {
+          r = KAPSM_ERR_CUDA;
+          break;
+        }
+        if ((r = Fns<T>::screen(rx, rx_stride, F, n_train, n_data, M, p, live_ws, s2))) break;
+        if (cudaEventRecord(join, s2) != cudaSuccess) { r = KAPSM_ERR_CUDA; break; }
+        if ((r = kapsm::train_tp(rx, rx_stride, pilots, F, K, n_train, M, window, eps, p, qtab,
+                                 gram_ws, coeff, first_step, theta, n_active, status, s)))
+          break;
+        goto finish;
+      }
+    }
+    if (false) goto finish;           // (the label is unused in the FP64 instantiation)
+    {
     const long long gstride = (long long)Np * ld;
     if ((r = Fns<T>::gram(rx, rx_stride, F, n_train, M, p, gram_ws, ld, gstride, stream))) break;
     // fork after K1: the screen then shares the GPU only with the trainer's
@@ -103,6 +174,8 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
                            Np, window, eps, p, qtab, nullptr, nullptr, coeff, first_step, theta,
                            n_active, status, stream)))
       break;
+    }
+  finish:
     if (bit_err && cudaMemsetAsync(bit_err, 0, sizeof(unsigned long long) * F * K, s) != cudaSuccess) {
       r = KAPSM_ERR_CUDA;
       break;
@@ -135,6 +208,28 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
   }
 KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f32, float)
 KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f64, double)
+
+// Internal (tests / A-B timing, not in the public header): the overlapped
+// pipeline in FP32 with the trainer forced -- mode 1: the Gram-based trainer
+// (K1 pilot Gram + K2 train.cu), mode 2: the one-warp-per-chain trainer
+// (train_tp.cu) whenever its limits hold, at any number of chains.
+extern "C" int kapsm_internal_run_frames_overlap_mode_f32(
+    int mode, const float* rx, long long rx_stride, const float* pilots,
+    const unsigned char* tx_labels, int F, int K, int n_train, int n_data, int M, int window,
+    double eps, kapsm_kernel_params p, const float* qtab, const float* points, int n_points,
+    int bps, float* gram_ws, long long ld, unsigned* live_ws, float* coeff, int* first_step,
+    float* theta, int* n_active, int* status, float* est, unsigned char* labels,
+    unsigned long long* bit_err, unsigned long long* sym_err, void* stream, void* side_stream) {
+#define KAPSM_MODE_CALL(MD)                                                                        \
+  return run_frames_overlap<float, MD>(rx, rx_stride, pilots, tx_labels, F, K, n_train, n_data, M, \
+                                       window, eps, p, qtab, points, n_points, bps, gram_ws, ld,   \
+                                       live_ws, coeff, first_step, theta, n_active, status, est,   \
+                                       labels, bit_err, sym_err, stream, side_stream)
+  if (mode == TRAINER_GRAM) KAPSM_MODE_CALL(TRAINER_GRAM);
+  if (mode == TRAINER_TP) KAPSM_MODE_CALL(TRAINER_TP);
+#undef KAPSM_MODE_CALL
+  return KAPSM_ERR_INVALID;
+}
 
 extern "C" int kapsm_stream_create(void** stream) {
   if (!stream) return KAPSM_ERR_INVALID;

@@ -119,7 +119,7 @@ struct TcSmem {
 template <int NT, int KC>
 __global__ void __launch_bounds__(TC_THREADS)
     detect_screen_tc_kernel(const float* __restrict__ rx, long long rx_stride, int n_train,
-                            int n_data, int M, float inv2s, float dead,
+                            int n_data, int y_row0, int M, float inv2s, float dead,
                             unsigned* __restrict__ live, int* __restrict__ cnt,
                             float4* __restrict__ vals) {
   using L = TcSmem<NT, KC>;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(TC_THREADS)
   const int D = 2 * M;
   const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
   const float* Xf = rx + (long long)f * rx_stride;
-  const float* Yf = Xf + (long long)n_train * D;
+  const float* Yf = Xf + (long long)y_row0 * D;           // the "payload" rows
   const int n_mt = (n_train + TC_MROWS - 1) / TC_MROWS;
 
   if (tid == 0) {
@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(TC_THREADS)
 
 template <int NT, int KC>
 static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data,
-                            int M, kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals,
-                            cudaStream_t s) {
+                            int y_row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
+                            float4* vals, cudaStream_t s) {
   const int NW = (n_train + 31) / 32;
   size_t smem = TcSmem<NT, KC>::bytes(NW);
   // at least 112 KB: never co-resident with a latency-mode trainer CTA (120 KB),
@@ -333,19 +333,31 @@ static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_t
       cudaSuccess)
     return KAPSM_ERR_CUDA;
   dim3 grid((n_data + NT - 1) / NT, F);
-  kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, M,
+  kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, y_row0, M,
                                       (float)(1.0 / (2.0 * p.sigma_sq)), 88.0f, live, cnt, vals);
   return status_from(cudaGetLastError());
 }
 
-// the tensor-core screen for M <= 64 (2M <= 128 floats per row); returns
+// the tensor-core screen for M <= 64 (2M <= 128 floats per row) of the pilots
+// against n_rows rows starting at row y_row0 of each frame (the payload for
+// the detection; the pilots themselves for the trainer's live lists);
 // KAPSM_ERR_UNSUPPORTED beyond (the caller keeps the SIMT screen)
+int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int n_rows,
+                   int y_row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
+                   float4* vals, cudaStream_t s) {
+#define KAPSM_TC(NT, KC)                                                                          \
+  return launch_screen_tc<NT, KC>(rx, rx_stride, F, n_train, n_rows, y_row0, M, p, live, cnt, \
+                                  vals, s)
+  if (M <= 16) KAPSM_TC(128, 1);
+  if (M <= 32) KAPSM_TC(128, 2);
+  if (M <= 64) KAPSM_TC(64, 4);
+#undef KAPSM_TC
+  return KAPSM_ERR_UNSUPPORTED;
+}
+
 int screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data, int M,
               kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals, cudaStream_t s) {
-  if (M <= 16) return launch_screen_tc<128, 1>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
-  if (M <= 32) return launch_screen_tc<128, 2>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
-  if (M <= 64) return launch_screen_tc<64, 4>(rx, rx_stride, F, n_train, n_data, M, p, live, cnt, vals, s);
-  return KAPSM_ERR_UNSUPPORTED;
+  return screen_tc_rows(rx, rx_stride, F, n_train, n_data, n_train, M, p, live, cnt, vals, s);
 }
 
 }  // namespace kapsm

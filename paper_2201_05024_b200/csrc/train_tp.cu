@@ -1,0 +1,495 @@
+// K2t: the APSM trainer as one warp per (frame, user) chain, for the frame
+// pipeline in FP32 (latency and throughput mode alike).
+//
+// Reference semantics: ApsmTrainer.observe (apsm.py:304-359) over the
+// realified pilots of the frame -- at step n the window J_n = [lo_n, n]
+// (apsm.py:132-136) gets
+//     delta_j = q_j / den_j * shrink(b_j - f_n(r_j), eps)   (apsm.py:323-336)
+//     c_j += delta_j, first activation = first n with delta_j != 0 (apsm.py:341-358)
+//     f_{n+1} = f_n + sum_j delta_j kappa(r_j, .)            (theta update, apsm.py:338)
+// with uniform weights q from the reference's own table (apsm.py:139-153).
+//
+// Restatement (exact algebra, FP32 rounding):
+//   * lane l of the warp owns ring slot l: sample m lives in slot m mod 32 from
+//     its takeover at step m - P (P = 28 - W) until it leaves the window after
+//     step m + W - 1.  Its response Y_m = f_n(r_m) is a register, updated each
+//     step by the window's deltas:  Y_m += sum_j delta_j K[j][m];
+//   * K[j][m] (sum kernel, w_l r.r + w_g kappa_G, explicit differences) for
+//     all ring pairs is a 32 x 32 shared matrix; a takeover writes the new
+//     sample's row and column from the band K[m][m-d], d < 32, made by
+//     band_kernel below (no pilot Gram matrix is materialised);
+//   * at takeover, f_{m-P}(r_m) = w_l theta_fin . r_m + sum_{j in window} c_j K[j][m]
+//       + w_g sum_{a <= m-P-W live} c_a kappa_G(r_a, r_m),
+//     theta_fin = sum of c_a r_a over the samples that already left the window
+//     (their coefficients are final; the linear part of every older sample),
+//     the window part from the band, and the older Gaussian terms from the
+//     live list of row m (the tensor-core screen on pilot x pilot pairs,
+//     screen_tc.cu: at the paper's channels the list is almost always empty);
+//   * theta = w_l theta_fin at the end (apsm.py:338 summed once per sample).
+// Global loads run two steps ahead with cp.async (a sample's pilot row, band
+// row, target and live count), so the chain never waits on memory.
+#include "kapsm_common.cuh"
+
+namespace kapsm {
+
+constexpr int TP_RING = 32;
+constexpr int TP_STG = 8;                // cp.async stages (power of 2, > TP_AHEAD)
+constexpr int TP_AHEAD = 6;              // prefetch distance (steps): hides a global-memory
+                                         // round trip behind ~6 chain steps
+constexpr int TP_LIVE_LAG = 2;           // live terms of a sample: 2 steps after its takeover
+constexpr int TP_CAP = 8;                // screen list entries per row (SC_CAP)
+
+constexpr int TP_SPAN = 28;              // P + W (< 32: slack for the live-term loads)
+__host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // takeover lead P
+
+// per-warp shared memory; a stage holds one sample's prefetched inputs:
+// pilot row (XR floats), band row (32), live-list row (8 float4), target, count
+__host__ __device__ constexpr int tp_xr(int D) { return (D + 3) & ~3; }
+__host__ __device__ constexpr int tp_sstr(int D) { return tp_xr(D) + 68; }
+struct TpSmem {
+  int ks, dsm, rr, stg, qs, total;
+  __host__ __device__ TpSmem(int D, int W) {
+    int o = 0;
+    auto take = [&](int bytes) { int r = o; o = (o + bytes + 15) & ~15; return r; };
+    ks = take(TP_RING * 33 * 4);
+    dsm = take(TP_RING * 4);
+    rr = take(TP_RING * D * 4);
+    stg = take(TP_STG * tp_sstr(D) * 4);
+    qs = take(2 * W * 4);
+    total = (o + 127) & ~127;
+  }
+};
+
+KAPSM_DEV void cpa16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+KAPSM_DEV void cpa4(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// K[m][m-d] for d = 0..31 (0 where m - d < 0): the band of the realified
+// pilot Gram that a chain's ring can meet.  Realified sample m = 2t + beta is
+// r1(x_t) (beta = 0) or r2(x_t) (beta = 1) of pilot x_t (apsm.py:156-182).
+// One thread per complex pilot pair (t, t - dt), dt = 0..16: one pass over the
+// antennas gives c = x^H y (y = x_t, x = x_{t-dt}) and the three distinct
+// distances |x - y|, |x + iy|, |x - iy| by explicit differences, hence the
+// 2 x 2 realified block: linear parts Re c, Im c, -Im c, Re c and Gaussian
+// parts of the matching distances (as screen.cu's list values).
+__global__ void __launch_bounds__(256)
+    band_kernel(const float* __restrict__ rx, long long rx_stride, int n_train, int M, float w_l,
+                float w_g, float inv2s, float* __restrict__ kband) {
+  const int Np = 2 * n_train, D = 2 * M;
+  const int f = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_train * 17) return;
+  const int t = i / 17, dt = i - t * 17, tp = t - dt;
+  float* kb = kband + (long long)f * Np * 32;
+  if (tp < 0) {                                           // before the first sample: zeros
+    for (int be = 0; be < 2; ++be)
+      for (int al = 0; al < 2; ++al) {
+        const int d = 2 * dt + be - al;
+        if (d >= 0 && d < 32) kb[(long long)(2 * t + be) * 32 + d] = 0.f;
+      }
+    return;
+  }
+  const float* X = rx + (long long)f * rx_stride;
+  const float* y = X + (long long)t * D;
+  const float* x = X + (long long)tp * D;
+  float cr = 0.f, ci = 0.f, ea = 0.f, eb = 0.f, ec = 0.f;
+  for (int k = 0; k < M; ++k) {
+    const float xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+    cr = fmaf(xr, yr, fmaf(xi, yi, cr));
+    ci = fmaf(xr, yi, fmaf(-xi, yr, ci));
+    float a0 = xr - yr, a1 = xi - yi;
+    ea = fmaf(a0, a0, fmaf(a1, a1, ea));
+    a0 = xr - yi; a1 = xi + yr;
+    eb = fmaf(a0, a0, fmaf(a1, a1, eb));
+    a0 = xr + yi; a1 = xi - yr;
+    ec = fmaf(a0, a0, fmaf(a1, a1, ec));
+  }
+  const bool gauss = w_g != 0.f;
+  const float ka = gauss ? (dt == 0 ? 1.f : exp_fast(-ea * inv2s)) : 0.f;
+  const float kbv = gauss ? exp_fast(-eb * inv2s) : 0.f;
+  const float kc = gauss ? exp_fast(-ec * inv2s) : 0.f;
+  // (alpha, beta) of a = 2(t - dt) + alpha, m = 2t + beta
+  const float v00 = w_l * cr + w_g * ka, v11 = v00;
+  const float v01 = w_l * ci + w_g * kbv;                 // r1(x) . r2(y) = Im(x^H y)
+  const float v10 = -w_l * ci + w_g * kc;                 // r2(x) . r1(y) = -Im(x^H y)
+  const float vals[2][2] = {{v00, v01}, {v10, v11}};      // [alpha][beta]
+  for (int be = 0; be < 2; ++be)
+    for (int al = 0; al < 2; ++al) {
+      const int d = 2 * dt + be - al;
+      if (d >= 0 && d < 32) kb[(long long)(2 * t + be) * 32 + d] = vals[al][be];
+    }
+}
+
+KAPSM_DEV float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// realified component e of sample (beta) from its interleaved pilot row x
+KAPSM_DEV float rcomp(const float* x, int e, int beta) {
+  if (!beta) return x[e];
+  return (e & 1) ? -x[e - 1] : x[e + 1];
+}
+
+template <int DPL>
+__global__ void __launch_bounds__(256)
+    apsm_train_tp_kernel(const float* __restrict__ rx, long long rx_stride,
+                         const float* __restrict__ targets, const float* __restrict__ kband,
+                         const unsigned* __restrict__ plive, const int* __restrict__ pcnt,
+                         const float4* __restrict__ pvals, int F, int K, int n_train, int M, int W,
+                         float eps, float w_l, float w_g, float inv2s,
+                         const float* __restrict__ qtab, float* __restrict__ coeff_out,
+                         int* __restrict__ fs_out, float* __restrict__ theta_out,
+                         int* __restrict__ nact_out, int* __restrict__ status_out) {
+  extern __shared__ __align__(128) unsigned char smem_tp[];
+  const int Np = 2 * n_train, D = 2 * M, P = tp_lead(W);
+  const TpSmem L(D, W);
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * wpc + warp;
+  if (task >= F * K) return;                    // warps are independent: no CTA barrier below
+  unsigned char* base = smem_tp + (size_t)warp * L.total;
+  const unsigned sbase = smem_u32(base);
+  float* Ks = reinterpret_cast<float*>(base + L.ks);       // [32][33] K over ring pairs
+  float* dsm = reinterpret_cast<float*>(base + L.dsm);     // [32] the step's deltas
+  float* Rr = reinterpret_cast<float*>(base + L.rr);       // [32][D] pilot rows of the ring
+  const float* Sg = reinterpret_cast<const float*>(base + L.stg);   // [STG][SSTR] stages
+  float* qs = reinterpret_cast<float*>(base + L.qs);       // [W][2] (q_mid, q_last)
+  const int XR = tp_xr(D), SSTR = tp_sstr(D);
+  const int f = task / K;
+  const float* X = rx + (long long)f * rx_stride;
+  const float* Bt = targets + (long long)task * Np;
+  const float* KB = kband + (long long)f * Np * 32;
+  const int NWp = (n_train + 31) / 32;
+  const unsigned* LW = plive + (long long)f * NWp * n_train;
+  const int* LC = pcnt + (long long)f * n_train;
+  const float4* LV = pvals + (long long)f * n_train * TP_CAP;
+  float* Cout = coeff_out + (long long)task * Np;
+  int* FSout = fs_out + (long long)task * Np;
+  const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
+  const bool gauss = w_g != 0.f;
+
+  for (int i = lane; i < TP_RING * 33; i += 32) Ks[i] = 0.f;
+  for (int i = lane; i < W; i += 32) {
+    qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
+    qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
+  }
+  dsm[lane] = 0.f;
+
+  // prefetch pieces of sample m into stage m mod STG (one cp.async group per
+  // step): the pilot row (16-byte pieces, or 4-byte ones when rows are not
+  // 16-byte aligned), the band row and the live-list row (8 pieces each), the
+  // target and the row's live count.  Each lane owns up to two pieces for the
+  // whole chain: global address g + m * gm + (m >> 1) * gt, shared address
+  // s + (m mod STG) * SSTR * 4, size 16 or 4 bytes (0: none).
+  const int XP = vec ? D / 4 : D, NPC = XP + 18;
+  const unsigned sg_s = sbase + L.stg;
+  const char* pg[2];
+  long long pgm[2], pgt[2];
+  unsigned ps[2];
+  int psz[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int pc = lane + 32 * r;
+    pg[r] = nullptr; pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0;
+    if (pc < XP) {
+      pg[r] = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
+      pgt[r] = (long long)D * 4;
+      ps[r] = sg_s + (unsigned)(vec ? 16 * pc : 4 * pc);
+      psz[r] = vec ? 16 : 4;
+    } else if (pc < XP + 8) {
+      const int q = pc - XP;
+      pg[r] = reinterpret_cast<const char*>(KB + 4 * q);
+      pgm[r] = 128;
+      ps[r] = sg_s + (unsigned)(XR + 4 * q) * 4;
+      psz[r] = 16;
+    } else if (pc < XP + 16) {
+      const int q = pc - XP - 8;
+      pg[r] = reinterpret_cast<const char*>(LV + q);
+      pgt[r] = (long long)TP_CAP * 16;
+      ps[r] = sg_s + (unsigned)(XR + 32 + 4 * q) * 4;
+      psz[r] = gauss ? 16 : 0;
+    } else if (pc == XP + 16) {
+      pg[r] = reinterpret_cast<const char*>(Bt);
+      pgm[r] = 4;
+      ps[r] = sg_s + (unsigned)(XR + 64) * 4;
+      psz[r] = 4;
+    } else if (pc == XP + 17) {
+      pg[r] = reinterpret_cast<const char*>(LC);
+      pgt[r] = 4;
+      ps[r] = sg_s + (unsigned)(XR + 65) * 4;
+      psz[r] = gauss ? 4 : 0;
+    }
+  }
+  const bool two = NPC > 32;
+  auto prefetch = [&](int m) {
+    const long long t = m >> 1;
+    const unsigned so = (unsigned)((m & (TP_STG - 1)) * SSTR) * 4;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r == 1 && !two) break;
+      const char* g = pg[r] + m * pgm[r] + t * pgt[r];
+      if (psz[r] == 16) cpa16(ps[r] + so, g);
+      else if (psz[r] == 4) cpa4(ps[r] + so, g);
+    }
+  };
+  for (int i = 0; i < TP_AHEAD; ++i) {
+    if (i < Np) prefetch(i);
+    cp_async_commit();
+  }
+
+  int samp = -(1 << 30);          // sample held by this lane's slot
+  float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
+  int fs = -1, nact = 0, status = 0;
+  double th[DPL];                 // theta_fin in FP64: 1400 accumulated updates, dotted with r
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) th[i] = 0.0;
+
+  for (int n = -P; n < Np; ++n) {
+    const int m = n + P;                        // taken over this step
+    cp_async_wait<TP_AHEAD - 1>();              // m's stage (issued TP_AHEAD steps ago) landed
+    __syncwarp();
+    // ---- live Gaussian terms of sample ml = m - 2: older samples, final c ----
+    const int ml = m - TP_LIVE_LAG;
+    if (gauss && ml >= 0 && ml < Np) {
+      const float* sl = Sg + (ml & (TP_STG - 1)) * SSTR;
+      const int cnt = __float_as_int(sl[XR + 65]);
+      const int bt = ml & 1;
+      float part = 0.f;
+      if (cnt > 0) {
+        if (lane < 2 * cnt) {
+          const float4 v4 = reinterpret_cast<const float4*>(sl + XR + 32)[lane >> 1];
+          const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
+          if (a <= ml - TP_SPAN) {
+            const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
+            part = w_g * __ldcg(Cout + a) * kap;
+          }
+        }
+      } else if (cnt < 0) {                     // more live pilots than the list holds
+        const int tl = ml >> 1;
+        const float* xm = X + (long long)tl * D;
+        for (int w = lane; w < NWp; w += 32) {
+          unsigned bits = LW[(long long)w * n_train + tl];
+          while (bits) {
+            const int p = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const float* xa = X + (long long)p * D;
+            for (int al = 0; al < 2; ++al) {
+              const int a = 2 * p + al;
+              if (a > ml - TP_SPAN) continue;
+              float dist = 0.f;
+              for (int e = 0; e < D; ++e) {
+                const float z = rcomp(xa, e, al) - rcomp(xm, e, bt);
+                dist = fmaf(z, z, dist);
+              }
+              part = fmaf(w_g * __ldcg(Cout + a), exp_fast(-dist * inv2s), part);
+            }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, part != 0.f)) {
+        part = warp_sum_f(part);
+        if (lane == (ml & 31)) Y += part;
+      }
+    }
+    // ---- takeover of sample m into slot sm ----
+    if (m < Np) {
+      const int sm = m & 31, bt = m & 1;
+      const float* sg = Sg + (m & (TP_STG - 1)) * SSTR;
+      const float v = sg[XR + ((sm - lane) & 31)];         // K[m][this lane's sample]
+      Ks[sm * 33 + lane] = v;
+      Ks[lane * 33 + sm] = v;
+      double part = 0.0;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int e = lane + 32 * i;
+        if (e < D) {
+          const float x0 = sg[e], x1 = sg[e ^ 1];
+          Rr[sm * D + e] = x0;                               // the ring keeps the pilot row
+          part = fma(th[i], (double)(bt ? ((e & 1) ? -x1 : x1) : x0), part);
+        }
+      }
+      float pf = (float)(part * (double)w_l);
+      const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);   // samp in [n-W+1, n-1]
+      pf = fmaf(win ? c : 0.f, v, pf);
+      const float init = warp_sum_f(pf);
+      const float b = sg[XR + 64];
+      const bool mine = lane == sm;             // this lane's slot takes sample m
+      samp = mine ? m : samp;
+      Y = mine ? init : Y;
+      c = mine ? 0.f : c;
+      fs = mine ? -1 : fs;
+      status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;   // kappa(r, r) = K[m][m]
+      const float rv = __frcp_rn(v);
+      idn = mine ? (v > 0.f ? rv : 0.f) : idn;
+      bl = mine ? b - eps : bl;
+      bh = mine ? b + eps : bh;
+    }
+    __syncwarp();                               // stage reads done before it is refilled
+    if (m + TP_AHEAD < Np) prefetch(m + TP_AHEAD);
+    cp_async_commit();
+    if (n < 0) continue;
+    // ---- step n: the window's deltas, then the window update ----
+    const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
+    const float qm = qs[2 * cj], ql = qs[2 * cj + 1];
+    const float q = samp == n ? ql : qm;
+    const bool inw = (unsigned)(samp - lo) <= (unsigned)cj;              // samp in [lo, n]
+    float dl = q * idn * (fmaxf(bl - Y, 0.f) + fminf(bh - Y, 0.f));
+    dl = inw ? dl : 0.f;
+    c += dl;
+    fs = (dl != 0.f && fs < 0) ? n : fs;
+    dsm[lane] = dl;
+    __syncwarp();                               // deltas and the takeover's K row/column
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int s = 0; s < 32; s += 4) {
+      const float4 dd = *reinterpret_cast<const float4*>(dsm + s);
+      a0 = fmaf(dd.x, Ks[s * 33 + lane], a0);
+      a1 = fmaf(dd.y, Ks[(s + 1) * 33 + lane], a1);
+      a2 = fmaf(dd.z, Ks[(s + 2) * 33 + lane], a2);
+      a3 = fmaf(dd.w, Ks[(s + 3) * 33 + lane], a3);
+    }
+    Y += (a0 + a1) + (a2 + a3);
+    // ---- the sample leaving after this step: its coefficient is final ----
+    const int a = n - W + 1;
+    if (a >= 0) {
+      const float ca = __shfl_sync(0xffffffffu, c, a & 31);
+      const float* xa = Rr + (a & 31) * D;
+      const int ba = a & 1;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int e = lane + 32 * i;
+        if (e < D) {
+          const float x0 = xa[e], x1 = xa[e ^ 1];
+          th[i] = fma((double)ca, (double)(ba ? ((e & 1) ? -x1 : x1) : x0), th[i]);
+        }
+      }
+      if (lane == (a & 31)) {
+        Cout[a] = c;
+        FSout[a] = fs;
+        nact += fs >= 0;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  // ---- samples still in the window after the last step ----
+  for (int a = (Np - W + 1 > 0 ? Np - W + 1 : 0); a < Np; ++a) {
+    const float ca = __shfl_sync(0xffffffffu, c, a & 31);
+    const float* xa = Rr + (a & 31) * D;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int e = lane + 32 * i;
+      if (e < D) th[i] = fma((double)ca, (double)rcomp(xa, e, a & 1), th[i]);
+    }
+    if (lane == (a & 31)) {
+      Cout[a] = c;
+      FSout[a] = fs;
+      nact += fs >= 0;
+    }
+  }
+  // theta = w_l theta_fin in the reference's block layout [Re; Im] (apsm.py:172-182)
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int e = lane + 32 * i;
+    if (e < D)
+      theta_out[(long long)task * D + ((e & 1) ? M + (e >> 1) : (e >> 1))] = (float)(w_l * th[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nact += __shfl_xor_sync(0xffffffffu, nact, o);
+    status |= __shfl_xor_sync(0xffffffffu, status, o);
+  }
+  if (lane == 0) {
+    nact_out[task] = nact;
+    status_out[task] = status;
+  }
+}
+
+static int tp_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int n_rows,
+                   int row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
+                   float4* vals, cudaStream_t s);
+
+// workspace carved out of the pipeline's Gram workspace: band rows, then the
+// pilot x pilot screen (live words, counts, lists)
+size_t train_tp_ws_bytes(int F, int n_train) {
+  const size_t Np = 2 * (size_t)n_train, NWp = (n_train + 31) / 32;
+  const size_t band = (F * Np * 32 * 4 + 255) / 256 * 256;
+  const size_t live = (F * NWp * n_train * 4 + 255) / 256 * 256;
+  const size_t cnt = (F * (size_t)n_train * 4 + 255) / 256 * 256;
+  return band + live + cnt + F * (size_t)n_train * TP_CAP * 16;
+}
+
+bool train_tp_supported(int n_train, int M, int W) {
+  // the live terms of a sample are added TP_AHEAD steps after its takeover, which
+  // must precede its entry into the window: P = TP_SPAN - W > TP_AHEAD
+  if (W < 1 || tp_lead(W) <= TP_AHEAD || M < 1 || M > 64 || n_train < 1) return false;
+  return TpSmem(2 * M, W).total <= 200 * 1024;
+}
+
+int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
+             int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
+             void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
+             cudaStream_t s) {
+  if (!train_tp_supported(n_train, M, W)) return KAPSM_ERR_UNSUPPORTED;
+  const int Np = 2 * n_train, NWp = (n_train + 31) / 32;
+  char* w = reinterpret_cast<char*>(ws);
+  float* kband = reinterpret_cast<float*>(w);
+  w += ((size_t)F * Np * 32 * 4 + 255) / 256 * 256;
+  unsigned* plive = reinterpret_cast<unsigned*>(w);
+  w += ((size_t)F * NWp * n_train * 4 + 255) / 256 * 256;
+  int* pcnt = reinterpret_cast<int*>(w);
+  w += ((size_t)F * n_train * 4 + 255) / 256 * 256;
+  float4* pvals = reinterpret_cast<float4*>(w);
+  const float inv2s = (float)(1.0 / (2.0 * p.sigma_sq));
+  {
+    dim3 grid((unsigned)((n_train * 17 + 255) / 256), F);
+    band_kernel<<<grid, 256, 0, s>>>(rx, rx_stride, n_train, M, (float)p.w_l, (float)p.w_g, inv2s,
+                                     kband);
+    if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
+  }
+  if (p.w_g != 0.0) {
+    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, M, p, plive, pcnt, pvals, s);
+    if (r) return r;
+  }
+  const TpSmem L(2 * M, W);
+  const int tasks = F * K;
+  // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
+  // so no other CTA (the concurrent detection screen) shares its SM;
+  // throughput: 4 chains per CTA (several CTAs per SM)
+  const bool lat = tasks <= tp_num_sms();
+  int wpc = lat ? 1 : 4;
+  while (wpc > 1 && (size_t)L.total * wpc > 227 * 1024) wpc >>= 1;
+  size_t smem = (size_t)L.total * wpc;
+  if (lat && smem < 120 * 1024) smem = 120 * 1024;
+  if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
+  const int DPL = (2 * M + 31) / 32;
+  auto launch = [&](auto kern) -> int {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return (int)KAPSM_ERR_CUDA;
+    kern<<<(tasks + wpc - 1) / wpc, 32 * wpc, smem, s>>>(
+        rx, rx_stride, targets, kband, plive, pcnt, pvals, F, K, n_train, M, W, (float)eps,
+        (float)p.w_l, (float)p.w_g, inv2s, qtab, coeff, first_step, theta, n_active, status);
+    return status_from(cudaGetLastError());
+  };
+  if (DPL == 1) return launch(apsm_train_tp_kernel<1>);
+  if (DPL == 2) return launch(apsm_train_tp_kernel<2>);
+  return launch(apsm_train_tp_kernel<4>);
+}
+
+}  // namespace kapsm

@@ -144,6 +144,16 @@ class FramePipeline:
         else:
             _lib.check(self._fn(*args, dv.stream()), "run_frames")
 
+    def launch_trainer(self, mode: int):
+        """Internal (tests, A/B timing): the overlapped FP32 pipeline with the
+        trainer forced -- 1: Gram-based (train.cu), 2: one warp per chain
+        (train_tp.cu) at any number of chains."""
+        if self.prec != "f32" or not self.overlap:
+            raise ValueError("launch_trainer needs the overlapped FP32 pipeline")
+        _lib.check(_lib.load().kapsm_internal_run_frames_overlap_mode_f32(
+            int(mode), *self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
+            "run_frames_overlap_mode")
+
     def launch(self):
         """Enqueue the whole pipeline on the current stream."""
         if self.overlap:
