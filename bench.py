@@ -448,32 +448,50 @@ def main():
     bit_err_last = int(sum(int(p.bit_err.sum().item()) for p in pipes))
 
     # ---------------- per-kernel times in one batch (roofline) ----------------
-    def kernel_times(pp, reps):
-        """Each stage of the pipeline alone on the launching stream (CUDA
-        events): pilot_gram, apsm_train, detect_screen, detect_finish."""
+    def ktime(fn, reps):
+        """Mean CUDA-event time (us) of fn() on the current stream."""
+        fn()
+        acc = 0.0
+        for _ in range(reps):
+            e0, e1 = ev(), ev()
+            e0.record(); fn(); e1.record(); e1.synchronize()
+            acc += e0.elapsed_time(e1)
+        return acc / reps * 1e3
+
+    def stage_fns(pp, batch_path):
+        """The pipeline's kernels as separate launches.  Batch (throughput)
+        path: band rows, pilot screen, one-warp-per-chain trainer, detection
+        screen, finish; single frame (latency) path: pilot Gram, Gram-based
+        trainer, detection screen, finish."""
         c = pp.cfg
         prm = _lib.params(c.params)
         st = dv.stream()
         F, T = pp.F, pp.T
-        acc = np.zeros(4)
-        for _ in range(reps):
-            e = [ev() for _ in range(5)]
-            e[0].record()
-            _lib.check(dv.fn("kapsm_pilot_gram", "f32")(dv.ptr(pp.rx), T * M_ANT * 2, F, N_TRAIN, M_ANT, prm, dv.ptr(pp.gram), pp.ld, pp.Np * pp.ld, st), "gram")
-            e[1].record()
-            _lib.check(dv.fn("kapsm_train", "f32")(dv.ptr(pp.gram), pp.ld, pp.Np * pp.ld, dv.ptr(pp.rx), T * M_ANT * 2, dv.ptr(None), 0, 2 * M_ANT, dv.ptr(pp.pilots), F, K_USERS, pp.Np, c.window, float(c.epsilon), prm, dv.ptr(pp.qtab), dv.ptr(None), dv.ptr(None), dv.ptr(pp.coeff), dv.ptr(pp.first_step), dv.ptr(pp.theta), dv.ptr(pp.n_active), dv.ptr(pp.status), st), "train")
-            e[2].record()
-            _lib.check(dv.fn("kapsm_detect_screen", "f32")(dv.ptr(pp.rx), T * M_ANT * 2, F, N_TRAIN, N_DATA, M_ANT, prm, dv.ptr(pp.live), st), "screen")
-            e[3].record()
-            _lib.check(dv.fn("kapsm_detect_finish", "f32")(dv.ptr(pp.rx), T * M_ANT * 2, F, K_USERS, N_TRAIN, N_DATA, M_ANT, dv.ptr(pp.coeff), dv.ptr(pp.theta), prm, dv.ptr(pp.points), pp.n_points, pp.bps, dv.ptr(pp.tx), dv.ptr(pp.live), dv.ptr(None), dv.ptr(pp.labels), dv.ptr(pp.bit_err), dv.ptr(pp.sym_err), st), "finish")
-            e[4].record()
-            e[4].synchronize()
-            acc += [e[i].elapsed_time(e[i + 1]) for i in range(4)]
-        return acc / reps * 1e3   # us
+        rxs = T * M_ANT * 2
+        fns = {}
+        if batch_path:
+            nb = int(lib.kapsm_internal_train_tp_ws_bytes(F, N_TRAIN))
+            ws = torch.empty(((nb + 15) // 16 * 4,), dtype=torch.int32, device=dev)
+
+            def tp(stage):
+                return lambda: _lib.check(lib.kapsm_internal_train_tp_f32(
+                    stage, dv.ptr(pp.rx), rxs, dv.ptr(pp.pilots), F, K_USERS, N_TRAIN, M_ANT,
+                    c.window, float(c.epsilon), prm, dv.ptr(pp.qtab), dv.ptr(ws), dv.ptr(pp.coeff),
+                    dv.ptr(pp.first_step), dv.ptr(pp.theta), dv.ptr(pp.n_active),
+                    dv.ptr(pp.status), st), "train_tp")
+            fns["band_rows"] = tp(1)
+            fns["pilot_screen_tc"] = tp(2)
+            fns["apsm_train_tp"] = tp(4)
+        else:
+            fns["pilot_gram"] = lambda: _lib.check(dv.fn("kapsm_pilot_gram", "f32")(dv.ptr(pp.rx), rxs, F, N_TRAIN, M_ANT, prm, dv.ptr(pp.gram), pp.ld, pp.Np * pp.ld, st), "gram")
+            fns["apsm_train"] = lambda: _lib.check(dv.fn("kapsm_train", "f32")(dv.ptr(pp.gram), pp.ld, pp.Np * pp.ld, dv.ptr(pp.rx), rxs, dv.ptr(None), 0, 2 * M_ANT, dv.ptr(pp.pilots), F, K_USERS, pp.Np, c.window, float(c.epsilon), prm, dv.ptr(pp.qtab), dv.ptr(None), dv.ptr(None), dv.ptr(pp.coeff), dv.ptr(pp.first_step), dv.ptr(pp.theta), dv.ptr(pp.n_active), dv.ptr(pp.status), st), "train")
+        fns["detect_screen_tc"] = lambda: _lib.check(dv.fn("kapsm_detect_screen", "f32")(dv.ptr(pp.rx), rxs, F, N_TRAIN, N_DATA, M_ANT, prm, dv.ptr(pp.live), st), "screen")
+        fns["detect_finish"] = lambda: _lib.check(dv.fn("kapsm_detect_finish", "f32")(dv.ptr(pp.rx), rxs, F, K_USERS, N_TRAIN, N_DATA, M_ANT, dv.ptr(pp.coeff), dv.ptr(pp.theta), prm, dv.ptr(pp.points), pp.n_points, pp.bps, dv.ptr(pp.tx), dv.ptr(pp.live), dv.ptr(None), dv.ptr(pp.labels), dv.ptr(pp.bit_err), dv.ptr(pp.sym_err), st), "finish")
+        return fns
 
     pipes[0].load(sl(rx_d, 0), sl(pil_d, 0), sl(tx_d, 0))
-    kt_batch = kernel_times(pipes[0], 5)
-    kt_one = kernel_times(pipe1, 20)
+    kt_batch = {n: ktime(f, 5) for n, f in stage_fns(pipes[0], True).items()}
+    kt_one = {n: ktime(f, 20) for n, f in stage_fns(pipe1, False).items()}
     del pipes
     torch.cuda.empty_cache()
 
@@ -490,26 +508,44 @@ def main():
     b.record()
     b.synchronize()
     fp32_peak = blocks * 256 * iters * 64 * 2 / (a.elapsed_time(b) / 1e3) / 1e12
+    # TF32 dense tensor peak: half the measured bf16 GEMM rate (MEASURED_PEAKS.json,
+    # burst figure -- the screens are timed alone); fallback per B200_PROFILING.md
+    peaks_src = "MEASURED_PEAKS.json bf16_tflops / 2"
+    try:
+        tf32_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] / 2
+    except Exception:
+        tf32_peak, peaks_src = 1590.0 / 2, "fallback 1.59 PFLOP/s bf16 / 2 (B200_PROFILING.md)"
 
     fl = flops_per_frame()
-    names = ["pilot_gram", "apsm_train", "detect_screen", "detect_finish"]
-    fkeys = ["gram", "train", "screen", "finish"]
+    D2 = 2 * M_ANT
+    # algorithmic work per frame of each kernel actually launched:
+    #  band rows   17 complex pairs per pilot: 2 complex-dot terms + 3 distances
+    #              by differences (26 flops per antenna) + 3 exps
+    #  screens     the TF32 cross-term GEMM: 2 x pilots x (2 x rows) x 2M
+    #  trainer     SURVEY 8(d) F_seq
+    #  finish      the linear part per user and payload realified sample
+    #              (2 K N_d D) -- the Gaussian part only over listed live pairs
+    work = {"band_rows": (N_TRAIN * 17 * (26 * M_ANT + 3), "fp32"),
+            "pilot_screen_tc": (2 * N_TRAIN * 2 * N_TRAIN * D2, "tensor_tf32"),
+            "apsm_train_tp": (fl["train"], "fp32"),
+            "pilot_gram": (fl["gram"], "fp32"),
+            "apsm_train": (fl["train"], "fp32"),
+            "detect_screen_tc": (2 * N_TRAIN * 2 * N_DATA * D2, "tensor_tf32"),
+            "detect_finish": (2 * K_USERS * 2 * N_DATA * D2, "fp32")}
 
     def per_kernel(kt, frames):
         out = {}
-        for n, t, k in zip(names, kt, fkeys):
-            tf = fl[k] * frames / (t / 1e6) / 1e12
-            out[n] = {"us": float(t), "algorithmic_gflop": fl[k] * frames / 1e9,
-                      "tflops": tf, "frac_of_fp32_peak": tf / fp32_peak}
-        scr = out["detect_screen"]
-        scr["executed_gflop"] = fl["screen_executed"] * frames / 1e9
-        scr["executed_frac_of_fp32_peak"] = (fl["screen_executed"] * frames / (scr["us"] / 1e6)
-                                             / 1e12 / fp32_peak)
+        for n, t in kt.items():
+            w, bound = work[n]
+            tf = w * frames / (t / 1e6) / 1e12
+            pk = tf32_peak if bound == "tensor_tf32" else fp32_peak
+            out[n] = {"us": float(t), "algorithmic_gflop": w * frames / 1e9, "bound": bound,
+                      "tflops": tf, "peak": pk, "frac": tf / pk}
         return out
 
     pk_batch = per_kernel(kt_batch, B)
     pk_one = per_kernel(kt_one, 1)
-    dom = names[int(np.argmax(kt_batch))]
+    dom = max(kt_batch, key=kt_batch.get)
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
@@ -517,24 +553,29 @@ def main():
             traffic = json.load(open(tr_path)).get(f"{dom}_batch{B}_bytes_per_launch")
         except Exception:
             traffic = None
-    frame_tflops = fl["total"] * value / world / 1e12
     # the single-frame trainer is a chain of 2 n_train dependent steps per user:
     # its floor is the bare per-step dependency chain (tools/micro/chain_bench.cu,
     # 106 cycles per step measured on B200), not FLOPs
     clk_mhz = clk.get("sm_mhz") or 1965.0
     chain_floor_us = 2 * N_TRAIN * 106 / clk_mhz
-    roofline = {"bound": "fp32", "kernel": dom, "achieved": pk_batch[dom]["tflops"],
-                "peak": fp32_peak, "unit": "TFLOP/s", "frac": pk_batch[dom]["frac_of_fp32_peak"],
-                "traffic": traffic,
-                "peak_source": "measured on this GPU (FFMA probe, 3-register form)",
+    roofline = {"bound": pk_batch[dom]["bound"], "kernel": dom,
+                "achieved": pk_batch[dom]["tflops"], "peak": pk_batch[dom]["peak"],
+                "unit": "TFLOP/s", "frac": pk_batch[dom]["frac"], "traffic": traffic,
+                "peak_source": ("fp32: measured on this GPU (FFMA probe, 3-register form); "
+                                f"tensor_tf32: {peaks_src}"),
                 "launch": f"{B} frames per launch (the bench step)",
-                "note": ("algorithmic FLOPs per SURVEY 8(d) minimal model x frames per launch / "
-                         "CUDA-event time of the launch; detect_screen runs concurrently with "
-                         "pilot_gram + apsm_train in the pipeline"),
+                "note": ("each kernel of the batch pipeline launched alone (CUDA events on its "
+                         "stream); algorithmic work per frame as listed in bench.py x frames "
+                         "per launch; in the pipeline the detection screen runs concurrently "
+                         "with the band, pilot screen and trainer"),
                 "kernels": pk_batch,
-                "frame_level": {"tflops": frame_tflops, "frac_of_fp32_peak":
-                                frame_tflops / fp32_peak,
-                                "gflop_per_frame": fl["total"] / 1e9},
+                "frame_level": {"credited_tflops": fl["total"] * value / world / 1e12,
+                                "gflop_per_frame": fl["total"] / 1e9,
+                                "note": ("SURVEY 8(d) minimal dense model (0.93 GFLOP/frame) x "
+                                         "frames/s; it credits the dense Gram and detection "
+                                         "contractions that the band rows, the tensor-core "
+                                         "screens and the live-pair finish do not execute, so "
+                                         "it can exceed the FP32 SIMT peak")},
                 "single_frame": {"kernels": pk_one,
                                  "apsm_train_chain_floor_us": chain_floor_us,
                                  "apsm_train_frac_of_chain_floor":
@@ -680,7 +721,7 @@ def main():
         others = other_configs()
 
     if rank == 0:
-        launches_per_step = 4      # pilot_gram, detect_screen, apsm_train, detect_finish
+        launches_per_step = 5      # band rows, pilot screen, trainer, detection screen, finish
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
               "steps": args.steps, "warmup": args.warmup,
               "ms_per_step": total_ms / args.steps, "higher_is_better": True,

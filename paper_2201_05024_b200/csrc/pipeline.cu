@@ -11,7 +11,7 @@ size_t train_tp_ws_bytes(int F, int n_train);
 int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
              int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
              void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
-             cudaStream_t s);
+             cudaStream_t s, int stages = 7);
 }  // namespace kapsm
 
 static int pipe_num_sms() {

@@ -441,10 +441,12 @@ bool train_tp_supported(int n_train, int M, int W) {
   return TpSmem(2 * M, W).total <= 200 * 1024;
 }
 
+// stages (bit mask, all by default): 1 band rows, 2 pilot screen, 4 trainer --
+// separate launches so the bench can time each on its stream
 int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
              int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
              void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
-             cudaStream_t s) {
+             cudaStream_t s, int stages = 7) {
   if (!train_tp_supported(n_train, M, W)) return KAPSM_ERR_UNSUPPORTED;
   const int Np = 2 * n_train, NWp = (n_train + 31) / 32;
   char* w = reinterpret_cast<char*>(ws);
@@ -456,16 +458,17 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
   w += ((size_t)F * n_train * 4 + 255) / 256 * 256;
   float4* pvals = reinterpret_cast<float4*>(w);
   const float inv2s = (float)(1.0 / (2.0 * p.sigma_sq));
-  {
+  if (stages & 1) {
     dim3 grid((unsigned)((n_train * 17 + 255) / 256), F);
     band_kernel<<<grid, 256, 0, s>>>(rx, rx_stride, n_train, M, (float)p.w_l, (float)p.w_g, inv2s,
                                      kband);
     if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
   }
-  if (p.w_g != 0.0) {
+  if ((stages & 2) && p.w_g != 0.0) {
     const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, M, p, plive, pcnt, pvals, s);
     if (r) return r;
   }
+  if (!(stages & 4)) return KAPSM_OK;
   const TpSmem L(2 * M, W);
   const int tasks = F * K;
   // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
@@ -493,3 +496,19 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
 }
 
 }  // namespace kapsm
+
+// Internal (bench stage timing, not in the public header): the throughput
+// trainer's stages alone -- band rows (1), pilot screen (2), trainer (4) -- on a
+// workspace of kapsm_internal_train_tp_ws_bytes bytes.
+extern "C" long long kapsm_internal_train_tp_ws_bytes(int F, int n_train) {
+  return (long long)kapsm::train_tp_ws_bytes(F, n_train);
+}
+extern "C" int kapsm_internal_train_tp_f32(int stages, const float* rx, long long rx_stride,
+                                           const float* targets, int F, int K, int n_train, int M,
+                                           int W, double eps, kapsm_kernel_params p,
+                                           const float* qtab, void* ws, float* coeff,
+                                           int* first_step, float* theta, int* n_active,
+                                           int* status, void* stream) {
+  return kapsm::train_tp(rx, rx_stride, targets, F, K, n_train, M, W, eps, p, qtab, ws, coeff,
+                         first_step, theta, n_active, status, (cudaStream_t)stream, stages);
+}
