@@ -42,18 +42,19 @@ constexpr int TP_CAP = 8;                // screen list entries per row (SC_CAP)
 constexpr int TP_SPAN = 28;              // P + W (< 32: slack for the live-term loads)
 __host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // takeover lead P
 
-// per-warp shared memory; a stage holds one sample's prefetched inputs:
-// pilot row (XR floats), band row (32), live-list row (8 float4), target, count
+// per-warp shared memory; the stage of step n = m - P holds the prefetched
+// inputs of that step: the pilot row of the sample taken over (m) and of the
+// sample leaving the window (m - TP_SPAN + 1), XR floats each, then the band
+// row (32), the live-list row (8 float4), the target and the live count
 __host__ __device__ constexpr int tp_xr(int D) { return (D + 3) & ~3; }
-__host__ __device__ constexpr int tp_sstr(int D) { return tp_xr(D) + 68; }
+__host__ __device__ constexpr int tp_sstr(int D) { return 2 * tp_xr(D) + 68; }
 struct TpSmem {
-  int ks, dsm, rr, stg, qs, total;
+  int ks, dsm, stg, qs, total;
   __host__ __device__ TpSmem(int D, int W) {
     int o = 0;
     auto take = [&](int bytes) { int r = o; o = (o + bytes + 15) & ~15; return r; };
     ks = take(TP_RING * 33 * 4);
     dsm = take(TP_RING * 4);
-    rr = take(TP_RING * D * 4);
     stg = take(TP_STG * tp_sstr(D) * 4);
     qs = take(2 * W * 4);
     total = (o + 127) & ~127;
@@ -155,10 +156,10 @@ __global__ void __launch_bounds__(256)
   const unsigned sbase = smem_u32(base);
   float* Ks = reinterpret_cast<float*>(base + L.ks);       // [32][33] K over ring pairs
   float* dsm = reinterpret_cast<float*>(base + L.dsm);     // [32] the step's deltas
-  float* Rr = reinterpret_cast<float*>(base + L.rr);       // [32][D] pilot rows of the ring
   const float* Sg = reinterpret_cast<const float*>(base + L.stg);   // [STG][SSTR] stages
   float* qs = reinterpret_cast<float*>(base + L.qs);       // [W][2] (q_mid, q_last)
   const int XR = tp_xr(D), SSTR = tp_sstr(D);
+  const int OKB = 2 * XR, OLV = OKB + 32, OB = OLV + 32, OLC = OB + 1;   // stage offsets
   const int f = task / K;
   const float* X = rx + (long long)f * rx_stride;
   const float* Bt = targets + (long long)task * Np;
@@ -185,68 +186,75 @@ __global__ void __launch_bounds__(256)
   // target and the row's live count.  Each lane owns up to two pieces for the
   // whole chain: global address g + m * gm + (m >> 1) * gt, shared address
   // s + (m mod STG) * SSTR * 4, size 16 or 4 bytes (0: none).
-  const int XP = vec ? D / 4 : D, NPC = XP + 18;
+  const int XP = vec ? D / 4 : D, NPC = 2 * XP + 18;
   const unsigned sg_s = sbase + L.stg;
-  const char* pg[2];
-  long long pgm[2], pgt[2];
-  unsigned ps[2];
-  int psz[2];
+  const char* pg[3];
+  long long pgm[3], pgt[3];
+  unsigned ps[3];
+  int psz[3], plv[3];            // plv: 1 = the leaving sample's row (row index m - SPAN + 1)
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int pc = lane + 32 * r;
-    pg[r] = nullptr; pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0;
-    if (pc < XP) {
+  for (int r = 0; r < 3; ++r) {
+    int pc = lane + 32 * r;
+    pg[r] = nullptr; pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; plv[r] = 0;
+    if (pc < 2 * XP) {
+      const int lv = pc >= XP;
+      if (lv) pc -= XP;
       pg[r] = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
       pgt[r] = (long long)D * 4;
-      ps[r] = sg_s + (unsigned)(vec ? 16 * pc : 4 * pc);
+      ps[r] = sg_s + (unsigned)(lv * XR + (vec ? 4 * pc : pc)) * 4;
       psz[r] = vec ? 16 : 4;
-    } else if (pc < XP + 8) {
-      const int q = pc - XP;
+      plv[r] = lv;
+    } else if (pc < 2 * XP + 8) {
+      const int q = pc - 2 * XP;
       pg[r] = reinterpret_cast<const char*>(KB + 4 * q);
       pgm[r] = 128;
-      ps[r] = sg_s + (unsigned)(XR + 4 * q) * 4;
+      ps[r] = sg_s + (unsigned)(OKB + 4 * q) * 4;
       psz[r] = 16;
-    } else if (pc < XP + 16) {
-      const int q = pc - XP - 8;
+    } else if (pc < 2 * XP + 16) {
+      const int q = pc - 2 * XP - 8;
       pg[r] = reinterpret_cast<const char*>(LV + q);
       pgt[r] = (long long)TP_CAP * 16;
-      ps[r] = sg_s + (unsigned)(XR + 32 + 4 * q) * 4;
+      ps[r] = sg_s + (unsigned)(OLV + 4 * q) * 4;
       psz[r] = gauss ? 16 : 0;
-    } else if (pc == XP + 16) {
+    } else if (pc == 2 * XP + 16) {
       pg[r] = reinterpret_cast<const char*>(Bt);
       pgm[r] = 4;
-      ps[r] = sg_s + (unsigned)(XR + 64) * 4;
+      ps[r] = sg_s + (unsigned)OB * 4;
       psz[r] = 4;
-    } else if (pc == XP + 17) {
+    } else if (pc == 2 * XP + 17) {
       pg[r] = reinterpret_cast<const char*>(LC);
       pgt[r] = 4;
-      ps[r] = sg_s + (unsigned)(XR + 65) * 4;
+      ps[r] = sg_s + (unsigned)OLC * 4;
       psz[r] = gauss ? 4 : 0;
     }
   }
-  const bool two = NPC > 32;
+  const int nr = (NPC + 31) / 32;
+  // stage of step m - P: sample m's pieces while m < Np, the leaving row
+  // (sample m - SPAN + 1) while that exists
   auto prefetch = [&](int m) {
-    const long long t = m >> 1;
+    const int ml = m - TP_SPAN + 1;
     const unsigned so = (unsigned)((m & (TP_STG - 1)) * SSTR) * 4;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (r == 1 && !two) break;
-      const char* g = pg[r] + m * pgm[r] + t * pgt[r];
+    for (int r = 0; r < 3; ++r) {
+      if (r >= nr) break;
+      const int mm = plv[r] ? ml : m;
+      if (mm < 0 || mm >= Np) continue;
+      const char* g = pg[r] + mm * pgm[r] + (long long)(mm >> 1) * pgt[r];
       if (psz[r] == 16) cpa16(ps[r] + so, g);
       else if (psz[r] == 4) cpa4(ps[r] + so, g);
     }
   };
   for (int i = 0; i < TP_AHEAD; ++i) {
-    if (i < Np) prefetch(i);
+    prefetch(i);
     cp_async_commit();
   }
 
   int samp = -(1 << 30);          // sample held by this lane's slot
   float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
   int fs = -1, nact = 0, status = 0;
-  double th[DPL];                 // theta_fin in FP64: 1400 accumulated updates, dotted with r
+  float th[DPL];
 #pragma unroll
-  for (int i = 0; i < DPL; ++i) th[i] = 0.0;
+  for (int i = 0; i < DPL; ++i) th[i] = 0.f;
 
   for (int n = -P; n < Np; ++n) {
     const int m = n + P;                        // taken over this step
@@ -256,12 +264,12 @@ __global__ void __launch_bounds__(256)
     const int ml = m - TP_LIVE_LAG;
     if (gauss && ml >= 0 && ml < Np) {
       const float* sl = Sg + (ml & (TP_STG - 1)) * SSTR;
-      const int cnt = __float_as_int(sl[XR + 65]);
+      const int cnt = __float_as_int(sl[OLC]);
       const int bt = ml & 1;
       float part = 0.f;
       if (cnt > 0) {
         if (lane < 2 * cnt) {
-          const float4 v4 = reinterpret_cast<const float4*>(sl + XR + 32)[lane >> 1];
+          const float4 v4 = reinterpret_cast<const float4*>(sl + OLV)[lane >> 1];
           const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
           if (a <= ml - TP_SPAN) {
             const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
@@ -296,27 +304,26 @@ __global__ void __launch_bounds__(256)
       }
     }
     // ---- takeover of sample m into slot sm ----
+    const float* sg = Sg + (m & (TP_STG - 1)) * SSTR;     // this step's stage
     if (m < Np) {
       const int sm = m & 31, bt = m & 1;
-      const float* sg = Sg + (m & (TP_STG - 1)) * SSTR;
-      const float v = sg[XR + ((sm - lane) & 31)];         // K[m][this lane's sample]
+      const float v = sg[OKB + ((sm - lane) & 31)];        // K[m][this lane's sample]
       Ks[sm * 33 + lane] = v;
       Ks[lane * 33 + sm] = v;
-      double part = 0.0;
+      float pf = 0.f;
 #pragma unroll
       for (int i = 0; i < DPL; ++i) {
         const int e = lane + 32 * i;
         if (e < D) {
           const float x0 = sg[e], x1 = sg[e ^ 1];
-          Rr[sm * D + e] = x0;                               // the ring keeps the pilot row
-          part = fma(th[i], (double)(bt ? ((e & 1) ? -x1 : x1) : x0), part);
+          pf = fmaf(th[i], bt ? ((e & 1) ? -x1 : x1) : x0, pf);
         }
       }
-      float pf = (float)(part * (double)w_l);
+      pf *= w_l;
       const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);   // samp in [n-W+1, n-1]
       pf = fmaf(win ? c : 0.f, v, pf);
       const float init = warp_sum_f(pf);
-      const float b = sg[XR + 64];
+      const float b = sg[OB];
       const bool mine = lane == sm;             // this lane's slot takes sample m
       samp = mine ? m : samp;
       Y = mine ? init : Y;
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(256)
       bh = mine ? b + eps : bh;
     }
     __syncwarp();                               // stage reads done before it is refilled
-    if (m + TP_AHEAD < Np) prefetch(m + TP_AHEAD);
+    prefetch(m + TP_AHEAD);
     cp_async_commit();
     if (n < 0) continue;
     // ---- step n: the window's deltas, then the window update ----
@@ -354,17 +361,16 @@ __global__ void __launch_bounds__(256)
     }
     Y += (a0 + a1) + (a2 + a3);
     // ---- the sample leaving after this step: its coefficient is final ----
-    const int a = n - W + 1;
+    const int a = n - W + 1;                    // == m - TP_SPAN + 1: its row is in the stage
     if (a >= 0) {
       const float ca = __shfl_sync(0xffffffffu, c, a & 31);
-      const float* xa = Rr + (a & 31) * D;
       const int ba = a & 1;
 #pragma unroll
       for (int i = 0; i < DPL; ++i) {
         const int e = lane + 32 * i;
         if (e < D) {
-          const float x0 = xa[e], x1 = xa[e ^ 1];
-          th[i] = fma((double)ca, (double)(ba ? ((e & 1) ? -x1 : x1) : x0), th[i]);
+          const float x0 = sg[XR + e], x1 = sg[XR + (e ^ 1)];
+          th[i] = fmaf(ca, ba ? ((e & 1) ? -x1 : x1) : x0, th[i]);
         }
       }
       if (lane == (a & 31)) {
@@ -376,14 +382,14 @@ __global__ void __launch_bounds__(256)
   }
   cp_async_wait<0>();
   __syncwarp();
-  // ---- samples still in the window after the last step ----
+  // ---- samples still in the window after the last step (rows from global) ----
   for (int a = (Np - W + 1 > 0 ? Np - W + 1 : 0); a < Np; ++a) {
     const float ca = __shfl_sync(0xffffffffu, c, a & 31);
-    const float* xa = Rr + (a & 31) * D;
+    const float* xa = X + (long long)(a >> 1) * D;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) {
       const int e = lane + 32 * i;
-      if (e < D) th[i] = fma((double)ca, (double)rcomp(xa, e, a & 1), th[i]);
+      if (e < D) th[i] = fmaf(ca, rcomp(xa, e, a & 1), th[i]);
     }
     if (lane == (a & 31)) {
       Cout[a] = c;
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < DPL; ++i) {
     const int e = lane + 32 * i;
     if (e < D)
-      theta_out[(long long)task * D + ((e & 1) ? M + (e >> 1) : (e >> 1))] = (float)(w_l * th[i]);
+      theta_out[(long long)task * D + ((e & 1) ? M + (e >> 1) : (e >> 1))] = w_l * th[i];
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
