@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--batch", type=int, default=256, help="frames per step per GPU")
+    ap.add_argument("--batch", type=int, default=1024, help="frames per step per GPU")
     ap.add_argument("--lat-samples", type=int, default=1000)
     ap.add_argument("--inflight", type=int, default=6,
                     help="single-frame streaming: frames in flight (FrameStream depth)")
@@ -357,15 +357,19 @@ def main():
         return 1
 
     # ---------------- frame pool (distinct seeds per rank, > L2) ----------------
+    # generated by a pool of host processes straight into pinned shared memory
+    # (framegen.FrameGenerator: two slots of B frames), copied once to the device
+    from paper_2201_05024_b200.framegen import FrameGenerator
     P = 2 * B
-    seeds = [rank * 1_000_000 + i for i in range(P)]
-    rx_h, pil_h, tx_h, _ = K.host_frames(seeds, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME)
-    rx_pin = torch.from_numpy(np.ascontiguousarray(
-        np.stack([rx_h.real, rx_h.imag], -1).astype(np.float32))).pin_memory()
-    pil_pin = torch.from_numpy(np.ascontiguousarray(
-        np.stack([pil_h.real, pil_h.imag], -1).astype(np.float32))).pin_memory()
-    tx_pin = torch.from_numpy(np.ascontiguousarray(tx_h.astype(np.uint8))).pin_memory()
-    del rx_h, pil_h, tx_h
+    gen_workers = max(1, cpu_cores() - 1)
+    t_gen = time.perf_counter()
+    gen = FrameGenerator(B, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, slots=2, workers=gen_workers)
+    for k in range(2):
+        gen.fill(k, [rank * 1_000_000 + k * B + i for i in range(B)]).wait()
+    t_gen = time.perf_counter() - t_gen
+    rx_pin = gen.rx.view(P, *gen.rx.shape[2:])
+    pil_pin = gen.pilots.view(P, *gen.pilots.shape[2:])
+    tx_pin = gen.tx.view(P, *gen.tx.shape[2:])
     rx_d, pil_d, tx_d = rx_pin.to(dev), pil_pin.to(dev), tx_pin.to(dev)
     frame_bytes = (rx_pin[0].numel() * 4 + pil_pin[0].numel() * 4 + tx_pin[0].numel())
 
@@ -667,6 +671,42 @@ def main():
     e2e_lat = np.array(e2e_lat)
     del fs
 
+    # ---------------- e2e with live generation ----------------
+    # the host pool generates batch i+1 into the other pinned slot while the GPU
+    # runs batch i; a slot is refilled only after its frames were consumed
+    # (their results are back).  Host-bound: the reference's numpy generator
+    # costs ~5.7 ms per frame per core.
+    live = None
+    if rank == 0:
+        L = 3
+        fsl = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32", depth=2,
+                            concurrent=True, frames=B)
+        seeds_live = lambda i: [rank * 1_000_000 + 500_000 + i * B + j for j in range(B)]  # noqa: E731
+        gen.fill(0, seeds_live(0)).wait()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tick = []
+        for i in range(L):
+            nxt = None
+            if i + 1 < L:
+                if i >= 1:
+                    fsl.done_event(tick[i - 1]).synchronize()     # slot (i+1)%2 consumed
+                nxt = gen.fill((i + 1) % 2, seeds_live(i + 1))
+            tick.append(fsl.submit(gen.rx[i % 2], gen.pilots[i % 2], gen.tx[i % 2]))
+            if nxt is not None:
+                nxt.wait()
+        fsl.done_event(tick[-1]).synchronize()
+        wall = time.perf_counter() - t0
+        be_live = int(fsl.result(tick[-1])[1].sum().item())
+        live = {"value": L * B / wall, "unit": UNIT, "frames": L * B, "workers": gen_workers,
+                "host_cores": cpu_cores(), "bit_errors_last_step": be_live,
+                "pool_generation_frames_per_s": P / t_gen,
+                "note": ("frames generated live by framegen.FrameGenerator (the reference's "
+                         "seeded numpy generator in worker processes, written into pinned "
+                         "shared memory) and streamed through FrameStream; wall clock over the "
+                         "whole run, host-generation bound")}
+        del fsl
+
     # ---------------- FP64 (the reference's own precision) ----------------
     fp64 = None
     if rank == 0:
@@ -720,6 +760,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_configs:
         others = other_configs()
 
+    gen.close()
     if rank == 0:
         launches_per_step = 5      # band rows, pilot screen, trainer, detection screen, finish
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -749,6 +790,7 @@ def main():
                       "api": (f"FrameStream(frames={B}, depth=2): pinned host batches, H2D / "
                               "compute / D2H overlapped across steps"),
                       "bit_errors_last_step": e2e_bit_err},
+              "e2e_live_generation": live,
               "fp64": fp64,
               "other_configs": others,
               "correctness_gate": gate,

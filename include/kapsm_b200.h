@@ -239,11 +239,18 @@ int kapsm_count_mismatch(const void* a, const void* b, long long n, int elem_byt
 /* ---------------------------------------------------------------------------
  * Whole frame pipeline on one stream: zero the counters, K1, K2, K3 for all K
  * users of F frames (run_trial, noma.py:249-281, once per target user).
- * gram_ws: workspace F x (2*n_train) x ld, ld >= 2*n_train + 16, followed by
- *          32 x ld zero elements (the trainer's staged reads run past the last
- *          sample into them).  Other arguments as
+ * gram_ws: workspace of kapsm_pipeline_workspace_bytes() bytes -- the pilot
+ *          Gram F x (2*n_train) x ld, ld = 2*n_train + 16 rounded up to 32,
+ *          followed by 32 x ld zero elements (the trainer's staged reads run
+ *          past the last sample into them); in FP32 throughput mode (more
+ *          chains than SMs, window <= 25, M <= 64) the band rows and pilot
+ *          screen of the one-warp-per-chain trainer instead.  Other arguments as
  * for the three stages.  Captured into a CUDA graph by the host.
  * ------------------------------------------------------------------------- */
+/* Bytes of gram_ws the pipelines need for this shape (elem_bytes 4: FP32,
+ * 8: FP64); -1 on invalid arguments. */
+long long kapsm_pipeline_workspace_bytes(int F, int K, int n_train, int M, int window,
+                                         int elem_bytes);
 int kapsm_run_frames_f32(const float* rx, long long rx_stride, const float* pilots,
                          const unsigned char* tx_labels, int F, int K, int n_train, int n_data,
                          int M, int window, double epsilon, kapsm_kernel_params p,

@@ -59,6 +59,7 @@ SIGNATURES = {
     "kapsm_run_frames_f64": (_I, [_P, _LL, _P, _P, _I, _I, _I, _I, _I, _I, _D, _KP, _P, _P, _I,
                                   _I, _P, _LL, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "kapsm_screen_workspace_bytes": (_LL, [_I, _I, _I]),
+    "kapsm_pipeline_workspace_bytes": (_LL, [_I, _I, _I, _I, _I, _I]),
     "kapsm_stream_create": (_I, [C.POINTER(C.c_void_p)]),
     "kapsm_stream_destroy": (_I, [_P]),
     "kapsm_stream_frame_in": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),

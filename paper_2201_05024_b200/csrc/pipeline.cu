@@ -36,15 +36,27 @@ enum TrainerMode { TRAINER_AUTO = 0, TRAINER_GRAM = 1, TRAINER_TP = 2 };
 template <typename T>
 static bool use_tp(int F, int K, int n_train, int M, int window, long long ld,
                    int mode = TRAINER_AUTO) {
+  (void)ld;
   if constexpr (sizeof(T) != 4) {
     return false;
   } else {
-    if (mode == TRAINER_GRAM) return false;
-    const size_t cap = ((size_t)F * 2 * n_train + 32) * (size_t)ld * sizeof(T);
-    const bool fits = kapsm::train_tp_supported(n_train, M, window) &&
-                      kapsm::train_tp_ws_bytes(F, n_train) <= cap;
-    return fits && (mode == TRAINER_TP || (long long)F * K > pipe_num_sms());
+    if (mode == TRAINER_GRAM || !kapsm::train_tp_supported(n_train, M, window)) return false;
+    return mode == TRAINER_TP || (long long)F * K > pipe_num_sms();
   }
+}
+
+// Bytes of gram_ws the pipeline needs: the one-warp trainer's workspace (band
+// rows + pilot screen) when it runs, else the pilot Gram F x Np x ld plus the
+// 32 zero tail rows (ld = Np rounded as below).  The caller allocates this.
+extern "C" long long kapsm_pipeline_workspace_bytes(int F, int K, int n_train, int M, int window,
+                                                    int elem_bytes) {
+  if (F < 0 || K < 1 || n_train < 1 || M < 1 || window < 1 || (elem_bytes != 4 && elem_bytes != 8))
+    return -1;
+  const long long Np = 2LL * n_train, ld = (Np + 16 + 31) / 32 * 32;
+  const long long gram = ((long long)F * Np + 32) * ld * elem_bytes;
+  if (elem_bytes == 4 && use_tp<float>(F, K, n_train, M, window, ld))
+    return (long long)kapsm::train_tp_ws_bytes(F, n_train);
+  return gram;
 }
 
 template <typename T> struct Fns;

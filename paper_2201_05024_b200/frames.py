@@ -37,7 +37,8 @@ def _ld(n: int) -> int:
 class FramePipeline:
     def __init__(self, F: int, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32",
-                 store_est: bool = True, device=None, overlap: bool = True):
+                 store_est: bool = True, device=None, overlap: bool = True,
+                 full_workspace: bool = False):
         if precision not in dv.DTYPES:
             raise ValueError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.cfg = cfg or ApsmConfig()
@@ -65,9 +66,19 @@ class FramePipeline:
         self.pilots = z(F, K, n_train, 2)
         self.tx = z(F, K, n_data, dt=torch.uint8)
         self.ld = _ld(self.Np)
-        # Gram workspace + the trainer's zero tail rows (kapsm_b200.h)
-        self._gram_buf = z(F * self.Np + 32, self.ld)
-        self.gram = self._gram_buf[: F * self.Np].view(F, self.Np, self.ld)
+        # trainer workspace (kapsm_pipeline_workspace_bytes): the pilot Gram +
+        # the trainer's zero tail rows, or in FP32 throughput mode the
+        # one-warp trainer's band rows + pilot screen; full_workspace keeps
+        # the Gram either way (``gram`` view; launch_trainer(1), stage timing)
+        esz = 4 if precision == "f32" else 8
+        ws = int(lib.kapsm_pipeline_workspace_bytes(F, K, n_train, M, self.cfg.window, esz))
+        full = (F * self.Np + 32) * self.ld * esz
+        if full_workspace or ws >= full:
+            self._gram_buf = z(F * self.Np + 32, self.ld)
+            self.gram = self._gram_buf[: F * self.Np].view(F, self.Np, self.ld)
+        else:
+            self._gram_buf = z((ws + esz * self.ld - 1) // (esz * self.ld), self.ld)
+            self.gram = None
         self.coeff = z(F, K, self.Np)
         self.first_step = z(F, K, self.Np, dt=torch.int32)
         self.theta = z(F, K, 2 * M)
@@ -118,7 +129,7 @@ class FramePipeline:
         head = (dv.ptr(rx), self.T * self.M * 2, dv.ptr(pilots), dv.ptr(tx),
                 self.F, self.K, self.n_train, self.n_data, self.M, c.window, float(c.epsilon),
                 _lib.params(c.params), dv.ptr(self.qtab), dv.ptr(self.points), self.n_points,
-                self.bps, dv.ptr(self.gram), self.ld)
+                self.bps, dv.ptr(self._gram_buf), self.ld)
         tail = (dv.ptr(self.coeff), dv.ptr(self.first_step), dv.ptr(self.theta),
                 dv.ptr(self.n_active), dv.ptr(self.status), dv.ptr(self.est),
                 dv.ptr(self.labels), dv.ptr(self.bit_err), dv.ptr(self.sym_err))
@@ -150,6 +161,8 @@ class FramePipeline:
         (train_tp.cu) at any number of chains."""
         if self.prec != "f32" or not self.overlap:
             raise ValueError("launch_trainer needs the overlapped FP32 pipeline")
+        if mode == 1 and self.gram is None:
+            raise ValueError("the Gram-based trainer needs FramePipeline(full_workspace=True)")
         _lib.check(_lib.load().kapsm_internal_run_frames_overlap_mode_f32(
             int(mode), *self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
             "run_frames_overlap_mode")

@@ -80,7 +80,7 @@ def test_tp_pipeline_matches_gram_pipeline(F):
     a.load(rx, pil, tx)
     a.launch_trainer(2)
     ra = a.results()
-    b = K.FramePipeline(F, 6, 16, 685, 3840, "QPSK", precision="f32")
+    b = K.FramePipeline(F, 6, 16, 685, 3840, "QPSK", precision="f32", full_workspace=True)
     b.load(rx, pil, tx)
     b.launch_trainer(1)
     rb = b.results()

@@ -9,7 +9,7 @@ F = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 CFG = {"C1": (6, 16, 685, 3840, "QPSK"), "C4": (16, 64, 685, 3840, "QAM16")}[sys.argv[2] if len(sys.argv) > 2 else "C1"]
 reps = 30
 rx, pil, tx, _ = K.host_frames(range(F), *CFG)
-pipe = K.FramePipeline(F, *CFG, precision="f32")
+pipe = K.FramePipeline(F, *CFG, precision="f32", full_workspace=True)
 pipe.load(rx, pil, tx)
 pipe.launch(); torch.cuda.synchronize()
 c = pipe.cfg; p = _lib.params(c.params); st = dv.stream(); gstride = pipe.Np * pipe.ld

@@ -9,7 +9,7 @@ g = np.load("tests/golden/c1_seeds20.npz")
 rx, pil, tx, _ = K.host_frames(range(20), 6, 16, 685, 3840, "QPSK")
 res = {}
 for mode in (1, 2):
-    p = K.FramePipeline(20, 6, 16, 685, 3840, "QPSK", precision="f32")
+    p = K.FramePipeline(20, 6, 16, 685, 3840, "QPSK", precision="f32", full_workspace=True)
     p.load(rx, pil, tx); p.launch_trainer(mode); res[mode] = p.results()
 for mode in (1, 2):
     r = res[mode]
@@ -19,7 +19,7 @@ for mode in (1, 2):
 seeds = list(range(50, 90))
 rx, pil, tx, _ = K.host_frames(seeds, 6, 16, 685, 3840, "QPSK")
 for mode in (1, 2):
-    p = K.FramePipeline(40, 6, 16, 685, 3840, "QPSK", precision="f32")
+    p = K.FramePipeline(40, 6, 16, 685, 3840, "QPSK", precision="f32", full_workspace=True)
     p.load(rx, pil, tx); p.launch_trainer(mode); res[mode] = p.results()
 bad = np.argwhere(res[1]["n_active"] != res[2]["n_active"])
 print("gram vs tp mismatches at seeds 50..89:", bad.tolist())
