@@ -77,42 +77,6 @@ struct WinBlocks {
   static constexpr bool blk(int b) { return in(4 * b) || in(4 * b + 1) || in(4 * b + 2) || in(4 * b + 3); }
 };
 
-template <int k, int WM>
-KAPSM_DEV float window_dot(unsigned dvb, const float (&row)[TC_S], float yz) {
-  using B = WinBlocks<k, WM>;
-  float2 a[4] = {make_float2(yz, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                 make_float2(0.f, 0.f)};
-  int ai = 0;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    if (B::blk(b)) {
-      const float4 v = lds_f4(dvb + 16 * b);
-      a[ai & 3] = __ffma2_rn(make_float2(v.x, v.y), make_float2(row[4 * b], row[4 * b + 1]), a[ai & 3]);
-      ++ai;
-      a[ai & 3] = __ffma2_rn(make_float2(v.z, v.w), make_float2(row[4 * b + 2], row[4 * b + 3]), a[ai & 3]);
-      ++ai;
-    }
-  }
-  const float2 s = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
-  return s.x + s.y;
-}
-template <int k, int WM>
-KAPSM_DEV double window_dot(unsigned dvb, const double (&row)[TC_S], double yz) {
-  using B = WinBlocks<k, WM>;
-  double a[4] = {yz, 0.0, 0.0, 0.0};
-  int ai = 0;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    if (B::blk(b)) {
-      const double2 v0 = lds_d2(dvb + 32 * b), v1 = lds_d2(dvb + 32 * b + 16);
-      a[ai & 3] = fma(v0.x, row[4 * b], a[ai & 3]); ++ai;
-      a[ai & 3] = fma(v0.y, row[4 * b + 1], a[ai & 3]); ++ai;
-      a[ai & 3] = fma(v1.x, row[4 * b + 2], a[ai & 3]); ++ai;
-      a[ai & 3] = fma(v1.y, row[4 * b + 3], a[ai & 3]); ++ai;
-    }
-  }
-  return (a[0] + a[1]) + (a[2] + a[3]);
-}
 
 // The broadcast deltas are stored rotated: lane x writes position
 // (x - k - 1) & 31 at step k, so the window lanes (k - j) & 31, j < WM,
@@ -147,24 +111,6 @@ KAPSM_DEV T window_fma(const typename WinLoad<T>::type (&wl)[8], const T (&row)[
     a[p & 3] = fma(w4(wl[p >> 2], p & 3), row[(p + k + 1) & (TC_S - 1)], a[p & 3]);
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
-// row[l] = buf[(l - c0) & 31], c0 a multiple of 4 (the staged segment's rotation)
-template <int c0>
-KAPSM_DEV void load_row32_rot(unsigned p, float (&r)[TC_S]) {
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 v = lds_f4(p + 4 * ((4 * q - c0) & (TC_S - 1)));
-    r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
-  }
-}
-template <int c0>
-KAPSM_DEV void load_row32_rot(unsigned p, double (&r)[TC_S]) {
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const unsigned o = p + 8 * ((4 * q - c0) & (TC_S - 1));
-    const double2 u = lds_d2(o), v = lds_d2(o + 16);
-    r[4 * q] = u.x; r[4 * q + 1] = u.y; r[4 * q + 2] = v.x; r[4 * q + 3] = v.y;
-  }
-}
 
 KAPSM_DEV void load_row32(unsigned p, float (&r)[TC_S]) {
 #pragma unroll
@@ -188,54 +134,6 @@ KAPSM_DEV float recip(float v) {   // MUFU.RCP (FP32 path tolerance is 1e-4)
 }
 KAPSM_DEV double recip(double v) { return 1.0 / v; }
 
-// Per-lane partial of sum_{i=0..last} c_i row[i], c_i read from the tagged
-// array (value, index); `bad` flags a coefficient that is not yet visible.
-// float: each lane takes 4 consecutive columns per LDS.128 (row) + 2 LDS.128 (tags).
-template <typename T>
-KAPSM_DEV T tagged_partial(const T* row, const typename Tagged<T>::slot_t* ctag, int last, int lane,
-                           bool& bad);
-template <>
-KAPSM_DEV float tagged_partial<float>(const float* row, const unsigned long long* ctag, int last,
-                                      int lane, bool& bad) {
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  const int n = last + 1;
-  int i = 4 * lane;
-#pragma unroll 4
-  for (; i + 3 < n; i += 128) {
-    const float4 r = *reinterpret_cast<const float4*>(row + i);
-    const uint4 t01 = *reinterpret_cast<const uint4*>(ctag + i);
-    const uint4 t23 = *reinterpret_cast<const uint4*>(ctag + i + 2);
-    bad |= (int)t01.y != i || (int)t01.w != i + 1 || (int)t23.y != i + 2 || (int)t23.w != i + 3;
-    s0 = fmaf(__uint_as_float(t01.x), r.x, s0);
-    s1 = fmaf(__uint_as_float(t01.z), r.y, s1);
-    s2 = fmaf(__uint_as_float(t23.x), r.z, s2);
-    s3 = fmaf(__uint_as_float(t23.z), r.w, s3);
-  }
-  for (int k = i; k < i + 4 && k < n; ++k) {      // ragged tail of this lane's block
-    const unsigned long long w = ctag[k];
-    bad |= (int)(w >> 32) != k;
-    s0 = fmaf(__uint_as_float((unsigned)(w & 0xffffffffu)), row[k], s0);
-  }
-  return (s0 + s1) + (s2 + s3);
-}
-template <>
-KAPSM_DEV double tagged_partial<double>(const double* row, const Tagged<double>::slot_t* ctag,
-                                        int last, int lane, bool& bad) {
-  double s0 = 0.0, s1 = 0.0;
-  int i = lane;
-  for (; i + 32 <= last; i += 64) {
-    const Tagged<double>::slot_t a = ctag[i], b = ctag[i + 32];
-    bad |= (int)a.t != i || (int)b.t != i + 32;
-    s0 = fma(__longlong_as_double((long long)a.v), row[i], s0);
-    s1 = fma(__longlong_as_double((long long)b.v), row[i + 32], s1);
-  }
-  if (i <= last) {
-    const Tagged<double>::slot_t a = ctag[i];
-    bad |= (int)a.t != i;
-    s0 = fma(__longlong_as_double((long long)a.v), row[i], s0);
-  }
-  return s0 + s1;
-}
 
 // 16-byte vectors for the background row dots
 template <typename T> struct Vec16;
@@ -246,12 +144,6 @@ KAPSM_DEV double2 ldg16(const double* p) { return __ldg(reinterpret_cast<const d
 template <typename T> KAPSM_DEV typename Vec16<T>::type lds16(unsigned a);
 template <> KAPSM_DEV float4 lds16<float>(unsigned a) { return lds_f4(a); }
 template <> KAPSM_DEV double2 lds16<double>(unsigned a) { return lds_d2(a); }
-KAPSM_DEV float dot16(const float4& c, const float4& r, float acc) {
-  return fmaf(c.w, r.w, fmaf(c.z, r.z, fmaf(c.y, r.y, fmaf(c.x, r.x, acc))));
-}
-KAPSM_DEV double dot16(const double2& c, const double2& r, double acc) {
-  return fma(c.y, r.y, fma(c.x, r.x, acc));
-}
 KAPSM_DEV float elem16(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 KAPSM_DEV double elem16(const double2& v, int e) { return e == 0 ? v.x : v.y; }
 
@@ -281,37 +173,6 @@ KAPSM_DEV double tagged_dot16<double>(unsigned a, int i0, const double2& r, doub
   return fma(v1, r.y, fma(v0, r.x, acc));
 }
 
-// Per-lane partial of sum_{i=0..last} c_i row[i] over plain arrays (the
-// caller has seen c_last published; earlier coefficients were stored first).
-KAPSM_DEV float plain_partial(const float* row, const float* cf, int last, int lane) {
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  const int n = last + 1;
-  int i = 4 * lane;
-#pragma unroll 4
-  for (; i + 3 < n; i += 128) {
-    const float4 r = *reinterpret_cast<const float4*>(row + i);
-    const float4 c = *reinterpret_cast<const float4*>(cf + i);
-    s0 = fmaf(c.x, r.x, s0);
-    s1 = fmaf(c.y, r.y, s1);
-    s2 = fmaf(c.z, r.z, s2);
-    s3 = fmaf(c.w, r.w, s3);
-  }
-  for (int k = i; k < i + 4 && k < n; ++k) s0 = fmaf(cf[k], row[k], s0);
-  return (s0 + s1) + (s2 + s3);
-}
-KAPSM_DEV double plain_partial(const double* row, const double* cf, int last, int lane) {
-  double s0 = 0.0, s1 = 0.0;
-  int i = 2 * lane;
-#pragma unroll 2
-  for (; i + 1 <= last; i += 64) {
-    const double2 r = *reinterpret_cast<const double2*>(row + i);
-    const double2 c = *reinterpret_cast<const double2*>(cf + i);
-    s0 = fma(c.x, r.x, s0);
-    s1 = fma(c.y, r.y, s1);
-  }
-  if (i <= last) s0 = fma(cf[i], row[i], s0);
-  return s0 + s1;
-}
 
 template <typename T>
 KAPSM_DEV T slot_value(const typename Tagged<T>::slot_t& w);
@@ -364,7 +225,6 @@ struct GroupSmem {
   // per-sample array (larger Np fits in shared memory)
   __host__ __device__ GroupSmem(int W, int Np, bool staged = false) {
     using Slot = typename Tagged<T>::slot_t;
-    constexpr int NB = Roles<NG, CL>::NB;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 15) & ~size_t(15); return r; };
     dv = take(2 * TC_S * sizeof(T));
