@@ -119,8 +119,8 @@ struct TcSmem {
 template <int NT, int KC>
 __global__ void __launch_bounds__(TC_THREADS)
     detect_screen_tc_kernel(const float* __restrict__ rx, long long rx_stride, int n_train,
-                            int n_data, int y_row0, int M, float inv2s, float dead,
-                            unsigned* __restrict__ live, int* __restrict__ cnt,
+                            int n_data, int y_row0, int list_max_off, int M, float inv2s,
+                            float dead, unsigned* __restrict__ live, int* __restrict__ cnt,
                             float4* __restrict__ vals) {
   using L = TcSmem<NT, KC>;
   extern __shared__ unsigned char smem_raw[];
@@ -282,46 +282,69 @@ __global__ void __launch_bounds__(TC_THREADS)
     const int w = i / NT, tt = t0 + (i - w * NT);
     if (tt < n_data) lf[(long long)w * n_data + tt] = bits[i];
   }
-  // ---- compact list of each symbol's live pilots in pilot order, kernel
-  //      values from explicit differences (kernels.py:187-191); more than
-  //      TC_CAP: count -1, the finish recomputes from the words ----
+  // ---- compact list of each symbol's live pilots in pilot order (those
+  //      with p <= t + list_max_off), kernel values from explicit differences
+  //      (kernels.py:187-191); more than TC_CAP: count -1, the consumer
+  //      recomputes from the words.  Phase 1: a thread per symbol gathers the
+  //      indices; phase 2: every thread takes (symbol, entry) items. ----
+  int* lp = reinterpret_cast<int*>(base + L::OFF_A);       // [NT][CAP] (A tiles are dead)
+  int* lnum = lp + NT * TC_CAP;                            // [NT]
   for (int r = tid; r < NT; r += TC_THREADS) {
     const int t = t0 + r;
-    if (t >= n_data) continue;
-    const float* y = Yf + (long long)t * D;
-    float4* vt = vals + ((long long)f * n_data + t) * TC_CAP;
     int j = 0;
-    for (int w = 0; w < NW; ++w) {
-      unsigned b = bits[w * NT + r];
-      while (b) {
-        const int pp = w * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        if (j < TC_CAP) {
-          const float* x = Xf + (long long)pp * D;
-          float ea = 0.f, eb = 0.f, ec = 0.f;
-          for (int k = 0; k < M; ++k) {
-            const float xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
-            float a0 = xr - yr, a1 = xi - yi;
-            ea = fmaf(a0, a0, fmaf(a1, a1, ea));
-            a0 = xr - yi; a1 = xi + yr;
-            eb = fmaf(a0, a0, fmaf(a1, a1, eb));
-            a0 = xr + yi; a1 = xi - yr;
-            ec = fmaf(a0, a0, fmaf(a1, a1, ec));
-          }
-          vt[j] = make_float4(exp_fast(-ea * inv2s), exp_fast(-eb * inv2s), exp_fast(-ec * inv2s),
-                              __int_as_float(pp));
+    if (t < n_data) {
+      const int pmax = t + list_max_off;
+      for (int w = 0; w < NW && w * 32 <= pmax; ++w) {
+        unsigned b = bits[w * NT + r];
+        while (b) {
+          const int pp = w * 32 + __ffs(b) - 1;
+          b &= b - 1;
+          if (pp > pmax) break;
+          if (j < TC_CAP) lp[r * TC_CAP + j] = pp;
+          ++j;
         }
-        ++j;
       }
+      cnt[(long long)f * n_data + t] = j <= TC_CAP ? j : -1;
     }
-    cnt[(long long)f * n_data + t] = j <= TC_CAP ? j : -1;
+    lnum[r] = j <= TC_CAP ? j : 0;
+  }
+  __syncthreads();
+  for (int it = tid; it < NT * TC_CAP; it += TC_THREADS) {
+    const int r = it / TC_CAP, j = it - r * TC_CAP;
+    if (j >= lnum[r]) continue;
+    const int t = t0 + r, pp = lp[it];
+    const float* x = Xf + (long long)pp * D;
+    const float* y = Yf + (long long)t * D;
+    float ea = 0.f, eb = 0.f, ec = 0.f;
+    auto acc = [&](float xr, float xi, float yr, float yi) {
+      float a0 = xr - yr, a1 = xi - yi;
+      ea = fmaf(a0, a0, fmaf(a1, a1, ea));
+      a0 = xr - yi; a1 = xi + yr;
+      eb = fmaf(a0, a0, fmaf(a1, a1, eb));
+      a0 = xr + yi; a1 = xi - yr;
+      ec = fmaf(a0, a0, fmaf(a1, a1, ec));
+    };
+    if (vec) {
+#pragma unroll 4
+      for (int q = 0; q < D / 4; ++q) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + q);
+        const float4 yv = __ldg(reinterpret_cast<const float4*>(y) + q);
+        acc(xv.x, xv.y, yv.x, yv.y);
+        acc(xv.z, xv.w, yv.z, yv.w);
+      }
+    } else {
+      for (int k = 0; k < M; ++k) acc(x[2 * k], x[2 * k + 1], y[2 * k], y[2 * k + 1]);
+    }
+    vals[((long long)f * n_data + t) * TC_CAP + j] =
+        make_float4(exp_fast(-ea * inv2s), exp_fast(-eb * inv2s), exp_fast(-ec * inv2s),
+                    __int_as_float(pp));
   }
 }
 
 template <int NT, int KC>
 static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data,
-                            int y_row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
-                            float4* vals, cudaStream_t s) {
+                            int y_row0, int list_max_off, int M, kapsm_kernel_params p,
+                            unsigned* live, int* cnt, float4* vals, cudaStream_t s) {
   const int NW = (n_train + 31) / 32;
   size_t smem = TcSmem<NT, KC>::bytes(NW);
   // at least 112 KB: never co-resident with a latency-mode trainer CTA (120 KB),
@@ -333,21 +356,22 @@ static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_t
       cudaSuccess)
     return KAPSM_ERR_CUDA;
   dim3 grid((n_data + NT - 1) / NT, F);
-  kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, y_row0, M,
+  kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, y_row0, list_max_off, M,
                                       (float)(1.0 / (2.0 * p.sigma_sq)), 88.0f, live, cnt, vals);
   return status_from(cudaGetLastError());
 }
 
 // the tensor-core screen for M <= 64 (2M <= 128 floats per row) of the pilots
 // against n_rows rows starting at row y_row0 of each frame (the payload for
-// the detection; the pilots themselves for the trainer's live lists);
-// KAPSM_ERR_UNSUPPORTED beyond (the caller keeps the SIMT screen)
+// the detection; the pilots themselves for the trainer's live lists, which
+// only need pilots p <= t + list_max_off of row t); KAPSM_ERR_UNSUPPORTED
+// beyond (the caller keeps the SIMT screen)
 int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int n_rows,
-                   int y_row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
-                   float4* vals, cudaStream_t s) {
-#define KAPSM_TC(NT, KC)                                                                          \
-  return launch_screen_tc<NT, KC>(rx, rx_stride, F, n_train, n_rows, y_row0, M, p, live, cnt, \
-                                  vals, s)
+                   int y_row0, int list_max_off, int M, kapsm_kernel_params p, unsigned* live,
+                   int* cnt, float4* vals, cudaStream_t s) {
+#define KAPSM_TC(NT, KC)                                                                   \
+  return launch_screen_tc<NT, KC>(rx, rx_stride, F, n_train, n_rows, y_row0, list_max_off, \
+                                  M, p, live, cnt, vals, s)
   if (M <= 16) KAPSM_TC(128, 1);
   if (M <= 32) KAPSM_TC(128, 2);
   if (M <= 64) KAPSM_TC(64, 4);
@@ -357,7 +381,8 @@ int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int
 
 int screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data, int M,
               kapsm_kernel_params p, unsigned* live, int* cnt, float4* vals, cudaStream_t s) {
-  return screen_tc_rows(rx, rx_stride, F, n_train, n_data, n_train, M, p, live, cnt, vals, s);
+  return screen_tc_rows(rx, rx_stride, F, n_train, n_data, n_train, 1 << 30, M, p, live, cnt,
+                        vals, s);
 }
 
 }  // namespace kapsm

@@ -38,6 +38,8 @@ constexpr int TP_AHEAD = 6;              // prefetch distance (steps): hides a g
                                          // round trip behind ~6 chain steps
 constexpr int TP_LIVE_LAG = 2;           // live terms of a sample: 2 steps after its takeover
 constexpr int TP_CAP = 8;                // screen list entries per row (SC_CAP)
+constexpr int TP_KS = 33;                // row stride of the ring's K matrix (odd: the
+                                         // takeover's column store is conflict-free)
 
 constexpr int TP_SPAN = 28;              // P + W (< 32: slack for the live-term loads)
 __host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // takeover lead P
@@ -53,7 +55,7 @@ struct TpSmem {
   __host__ __device__ TpSmem(int D, int W) {
     int o = 0;
     auto take = [&](int bytes) { int r = o; o = (o + bytes + 15) & ~15; return r; };
-    ks = take(TP_RING * 33 * 4);
+    ks = take(TP_RING * TP_KS * 4);
     dsm = take(TP_RING * 4);
     stg = take(TP_STG * tp_sstr(D) * 4);
     qs = take(2 * W * 4);
@@ -137,7 +139,7 @@ KAPSM_DEV float rcomp(const float* x, int e, int beta) {
 }
 
 template <int DPL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128, 6)
     apsm_train_tp_kernel(const float* __restrict__ rx, long long rx_stride,
                          const float* __restrict__ targets, const float* __restrict__ kband,
                          const unsigned* __restrict__ plive, const int* __restrict__ pcnt,
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(256)
   if (task >= F * K) return;                    // warps are independent: no CTA barrier below
   unsigned char* base = smem_tp + (size_t)warp * L.total;
   const unsigned sbase = smem_u32(base);
-  float* Ks = reinterpret_cast<float*>(base + L.ks);       // [32][33] K over ring pairs
+  float* Ks = reinterpret_cast<float*>(base + L.ks);       // [32][TP_KS] K over ring pairs
   float* dsm = reinterpret_cast<float*>(base + L.dsm);     // [32] the step's deltas
   const float* Sg = reinterpret_cast<const float*>(base + L.stg);   // [STG][SSTR] stages
   float* qs = reinterpret_cast<float*>(base + L.qs);       // [W][2] (q_mid, q_last)
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(256)
   const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
   const bool gauss = w_g != 0.f;
 
-  for (int i = lane; i < TP_RING * 33; i += 32) Ks[i] = 0.f;
+  for (int i = lane; i < TP_RING * TP_KS; i += 32) Ks[i] = 0.f;
   for (int i = lane; i < W; i += 32) {
     qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
     qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
@@ -230,7 +232,8 @@ __global__ void __launch_bounds__(256)
   }
   const int nr = (NPC + 31) / 32;
   // stage of step m - P: sample m's pieces while m < Np, the leaving row
-  // (sample m - SPAN + 1) while that exists
+  // (sample m - SPAN + 1) while that exists.  Each role's global address is
+  // g + mm * gm + (mm >> 1) * gt for its sample mm.
   auto prefetch = [&](int m) {
     const int ml = m - TP_SPAN + 1;
     const unsigned so = (unsigned)((m & (TP_STG - 1)) * SSTR) * 4;
@@ -308,8 +311,8 @@ __global__ void __launch_bounds__(256)
     if (m < Np) {
       const int sm = m & 31, bt = m & 1;
       const float v = sg[OKB + ((sm - lane) & 31)];        // K[m][this lane's sample]
-      Ks[sm * 33 + lane] = v;
-      Ks[lane * 33 + sm] = v;
+      Ks[sm * TP_KS + lane] = v;                           // K is symmetric: row and column
+      Ks[lane * TP_KS + sm] = v;
       float pf = 0.f;
 #pragma unroll
       for (int i = 0; i < DPL; ++i) {
@@ -354,10 +357,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int s = 0; s < 32; s += 4) {
       const float4 dd = *reinterpret_cast<const float4*>(dsm + s);
-      a0 = fmaf(dd.x, Ks[s * 33 + lane], a0);
-      a1 = fmaf(dd.y, Ks[(s + 1) * 33 + lane], a1);
-      a2 = fmaf(dd.z, Ks[(s + 2) * 33 + lane], a2);
-      a3 = fmaf(dd.w, Ks[(s + 3) * 33 + lane], a3);
+      a0 = fmaf(dd.x, Ks[s * TP_KS + lane], a0);
+      a1 = fmaf(dd.y, Ks[(s + 1) * TP_KS + lane], a1);
+      a2 = fmaf(dd.z, Ks[(s + 2) * TP_KS + lane], a2);
+      a3 = fmaf(dd.w, Ks[(s + 3) * TP_KS + lane], a3);
     }
     Y += (a0 + a1) + (a2 + a3);
     // ---- the sample leaving after this step: its coefficient is final ----
@@ -427,8 +430,8 @@ static int tp_num_sms() {
 }
 
 int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int n_rows,
-                   int row0, int M, kapsm_kernel_params p, unsigned* live, int* cnt,
-                   float4* vals, cudaStream_t s);
+                   int y_row0, int list_max_off, int M, kapsm_kernel_params p, unsigned* live,
+                   int* cnt, float4* vals, cudaStream_t s);
 
 // workspace carved out of the pipeline's Gram workspace: band rows, then the
 // pilot x pilot screen (live words, counts, lists)
@@ -471,7 +474,10 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
     if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
   }
   if ((stages & 2) && p.w_g != 0.0) {
-    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, M, p, plive, pcnt, pvals, s);
+    // lists only hold pilots p <= t - TP_SPAN / 2 of row t: the trainer's live
+    // terms are the samples a <= m - TP_SPAN (the band rows cover the rest)
+    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, -(TP_SPAN / 2), M, p,
+                                 plive, pcnt, pvals, s);
     if (r) return r;
   }
   if (!(stages & 4)) return KAPSM_OK;
