@@ -99,8 +99,7 @@ __global__ void __launch_bounds__(256)
   const float* y = X + (long long)t * D;
   const float* x = X + (long long)tp * D;
   float cr = 0.f, ci = 0.f, ea = 0.f, eb = 0.f, ec = 0.f;
-  for (int k = 0; k < M; ++k) {
-    const float xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
+  auto acc = [&](float xr, float xi, float yr, float yi) {
     cr = fmaf(xr, yr, fmaf(xi, yi, cr));
     ci = fmaf(xr, yi, fmaf(-xi, yr, ci));
     float a0 = xr - yr, a1 = xi - yi;
@@ -109,6 +108,17 @@ __global__ void __launch_bounds__(256)
     eb = fmaf(a0, a0, fmaf(a1, a1, eb));
     a0 = xr + yi; a1 = xi - yr;
     ec = fmaf(a0, a0, fmaf(a1, a1, ec));
+  };
+  if ((D & 3) == 0 && (rx_stride & 3) == 0 && ((size_t)rx & 15) == 0) {
+#pragma unroll 8
+    for (int q = 0; q < D / 4; ++q) {            // 16-byte loads: two antennas each
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + q);
+      const float4 yv = __ldg(reinterpret_cast<const float4*>(y) + q);
+      acc(xv.x, xv.y, yv.x, yv.y);
+      acc(xv.z, xv.w, yv.z, yv.w);
+    }
+  } else {
+    for (int k = 0; k < M; ++k) acc(x[2 * k], x[2 * k + 1], y[2 * k], y[2 * k + 1]);
   }
   const bool gauss = w_g != 0.f;
   const float ka = gauss ? (dt == 0 ? 1.f : exp_fast(-ea * inv2s)) : 0.f;
