@@ -69,6 +69,29 @@ KAPSM_DEV void cpa16(unsigned dst, const void* src) {
 KAPSM_DEV void cpa4(unsigned dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
+// predicated forms (no branch in the chain's loop)
+KAPSM_DEV void cpa16_if(bool p, unsigned dst, const void* src) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+               "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}"
+               ::"r"(dst), "l"(src), "r"((int)p) : "memory");
+}
+KAPSM_DEV void cpa4_if(bool p, unsigned dst, const void* src) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+               "@q cp.async.ca.shared.global [%0], [%1], 4;\n\t}"
+               ::"r"(dst), "l"(src), "r"((int)p) : "memory");
+}
+template <typename V>
+KAPSM_DEV void stg_if(bool p, V* dst, V v);
+template <>
+KAPSM_DEV void stg_if<float>(bool p, float* dst, float v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}"
+               ::"l"(dst), "f"(v), "r"((int)p) : "memory");
+}
+template <>
+KAPSM_DEV void stg_if<int>(bool p, int* dst, int v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.s32 [%0], %1;\n\t}"
+               ::"l"(dst), "r"(v), "r"((int)p) : "memory");
+}
 
 // K[m][m-d] for d = 0..31 (0 where m - d < 0): the band of the realified
 // pilot Gram that a chain's ring can meet.  Realified sample m = 2t + beta is
@@ -249,12 +272,14 @@ __global__ void __launch_bounds__(128, 6)
     const unsigned so = (unsigned)((m & (TP_STG - 1)) * SSTR) * 4;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      if (r >= nr) break;
-      const int mm = plv[r] ? ml : m;
-      if (mm < 0 || mm >= Np) continue;
-      const char* g = pg[r] + mm * pgm[r] + (long long)(mm >> 1) * pgt[r];
-      if (psz[r] == 16) cpa16(ps[r] + so, g);
-      else if (psz[r] == 4) cpa4(ps[r] + so, g);
+      if (r < nr) {
+        const int mm = plv[r] ? ml : m;
+        const bool go = (unsigned)mm < (unsigned)Np;
+        const int mc = go ? mm : 0;
+        const char* g = pg[r] + mc * pgm[r] + (long long)(mc >> 1) * pgt[r];
+        cpa16_if(go && psz[r] == 16, ps[r] + so, g);
+        cpa4_if(go && psz[r] == 4, ps[r] + so, g);
+      }
     }
   };
   for (int i = 0; i < TP_AHEAD; ++i) {
@@ -386,11 +411,10 @@ __global__ void __launch_bounds__(128, 6)
           th[i] = fmaf(ca, ba ? ((e & 1) ? -x1 : x1) : x0, th[i]);
         }
       }
-      if (lane == (a & 31)) {
-        Cout[a] = c;
-        FSout[a] = fs;
-        nact += fs >= 0;
-      }
+      const bool own = lane == (a & 31);
+      stg_if(own, Cout + a, c);
+      stg_if(own, FSout + a, fs);
+      nact += (own && fs >= 0) ? 1 : 0;
     }
   }
   cp_async_wait<0>();
