@@ -361,7 +361,7 @@ def main():
     # (framegen.FrameGenerator: two slots of B frames), copied once to the device
     from paper_2201_05024_b200.framegen import FrameGenerator
     P = 2 * B
-    gen_workers = max(1, cpu_cores() - 1)
+    gen_workers = max(1, cpu_cores() // world - 1)     # the host's cores shared by the ranks
     t_gen = time.perf_counter()
     gen = FrameGenerator(B, K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, slots=2, workers=gen_workers)
     for k in range(2):
