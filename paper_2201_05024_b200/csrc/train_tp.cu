@@ -38,8 +38,8 @@ constexpr int TP_AHEAD = 6;              // prefetch distance (steps): hides a g
                                          // round trip behind ~6 chain steps
 constexpr int TP_LIVE_LAG = 2;           // live terms of a sample: 2 steps after its takeover
 constexpr int TP_CAP = 8;                // screen list entries per row (SC_CAP)
-constexpr int TP_KS = 33;                // row stride of the ring's K matrix (odd: the
-                                         // takeover's column store is conflict-free)
+constexpr int TP_KS = 36;                // row stride of the ring's K matrix: 16-byte rows
+                                         // whose LDS.128 phases hit distinct banks
 
 constexpr int TP_SPAN = 28;              // P + W (< 32: slack for the live-term loads)
 __host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // takeover lead P
@@ -389,13 +389,16 @@ __global__ void __launch_bounds__(128, 6)
     dsm[lane] = dl;
     __syncwarp();                               // deltas and the takeover's K row/column
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    const unsigned krow = sbase + L.ks + (unsigned)(lane * TP_KS) * 4;   // K[.][my sample]
+    const unsigned dsa = sbase + L.dsm;
 #pragma unroll
     for (int s = 0; s < 32; s += 4) {
-      const float4 dd = *reinterpret_cast<const float4*>(dsm + s);
-      a0 = fmaf(dd.x, Ks[s * TP_KS + lane], a0);
-      a1 = fmaf(dd.y, Ks[(s + 1) * TP_KS + lane], a1);
-      a2 = fmaf(dd.z, Ks[(s + 2) * TP_KS + lane], a2);
-      a3 = fmaf(dd.w, Ks[(s + 3) * TP_KS + lane], a3);
+      const float4 dd = lds_f4(dsa + 4u * s);
+      const float4 kk = lds_f4(krow + 4u * s);
+      a0 = fmaf(dd.x, kk.x, a0);
+      a1 = fmaf(dd.y, kk.y, a1);
+      a2 = fmaf(dd.z, kk.z, a2);
+      a3 = fmaf(dd.w, kk.w, a3);
     }
     Y += (a0 + a1) + (a2 + a3);
     // ---- the sample leaving after this step: its coefficient is final ----

@@ -458,3 +458,33 @@ def test_launch_on_device_frames_in_place():
     assert np.array_equal(got["est"], ref["est"])
     with pytest.raises(ValueError):
         q.launch_on(rx_d.double(), pil_d, tx_d)
+
+
+def test_frame_stream_batches_throughput_mode():
+    """FrameStream(frames=F) with F x K > SMs (the bench's e2e path: the
+    one-warp trainer inside the captured pipelines), fed from the pinned ring
+    of FrameGenerator: every batch's decisions and counts equal one
+    FramePipeline launch per batch."""
+    from paper_2201_05024_b200.framegen import FrameGenerator
+    F, Kk, M, nt, nd = 30, 6, 16, 200, 160          # 180 chains > 148 SMs
+    gen = FrameGenerator(F, Kk, M, nt, nd, "QPSK", slots=2, workers=2)
+    try:
+        fs = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=2, concurrent=True, frames=F)
+        seeds = [list(range(700 + F * b, 700 + F * (b + 1))) for b in range(3)]
+        out = []
+        for b in range(3):
+            gen.fill(b % 2, seeds[b]).wait()
+            t = fs.submit(gen.rx[b % 2], gen.pilots[b % 2], gen.tx[b % 2])
+            lab, be, se = fs.result(t)
+            out.append((lab.clone(), be.clone(), se.clone()))
+        for b in range(3):
+            rx, pil, tx, _ = K.host_frames(seeds[b], Kk, M, nt, nd, "QPSK")
+            ref = K.FramePipeline(F, Kk, M, nt, nd, "QPSK", precision="f32", store_est=False)
+            ref.load(rx, pil, tx)
+            ref.launch()
+            r = ref.results(est=False)
+            assert np.array_equal(out[b][0].numpy(), r["labels"])
+            assert np.array_equal(out[b][1].numpy(), r["bit_err"])
+            assert np.array_equal(out[b][2].numpy(), r["sym_err"])
+    finally:
+        gen.close()
