@@ -215,9 +215,11 @@ __global__ void __launch_bounds__(SC_WARPS * 32)
 
 // One thread per (payload symbol, user): linear part, the live pilots (their
 // words prefetched together), demap, counts.  Threads of the same payload
-// symbol share the live words and the pilot rows through L1.
+// symbol share the live words and the pilot rows through L1; a CTA holds 32
+// symbols x up to 8 users (all users at the paper's K = 6: the payload rows
+// are staged once per frame), 4 users for the wide rows of M > 16.
 template <typename T, int MT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     detect_finish_kernel(const T* __restrict__ rx, long long rx_stride, int K, int n_train,
                          int n_data, int M, const T* __restrict__ coeff,
                          const T* __restrict__ theta, T w_g, T inv2s,
@@ -245,7 +247,37 @@ __global__ void __launch_bounds__(128)
   {
     const int t0 = blockIdx.x * 32, rows = min(32, n_data - t0), rl = 2 * M;
     const T* src = Xf + (long long)(n_train + t0) * rl;
-    for (int e = tid; e < rows * rl; e += nthr) ys[(e / rl) * YS + e % rl] = src[e];
+    // all loads of a thread issued before its stores (one memory latency),
+    // 16-byte pieces of the 32 contiguous rows of rl = 2M elements
+    const int n = rows * rl;
+    if (sizeof(T) == 4 && (rl & 3) == 0 && ((size_t)src & 15) == 0) {
+      constexpr int PER = (32 * 2 * MT / 4 + 127) / 128;  // float4 per thread at >= 128 threads
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4 v[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int e4 = tid + i * nthr;
+        v[i] = 4 * e4 < n ? __ldg(s4 + e4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int e = 4 * (tid + i * nthr);
+        if (e < n) {
+          const int r = e / rl, c = e - r * rl;
+          T* d = ys + r * YS + c;
+          d[0] = (T)v[i].x; d[1] = (T)v[i].y; d[2] = (T)v[i].z; d[3] = (T)v[i].w;
+        }
+      }
+      for (int e = 4 * (tid + PER * nthr); e < n; e += 4 * nthr) {   // (< 128 threads)
+        const int r = e / rl, c = e - r * rl;
+        for (int j = 0; j < 4; ++j) ys[r * YS + c + j] = src[e + j];
+      }
+    } else {
+      for (int e = tid; e < n; e += nthr) {
+        const int r = e / rl;
+        ys[r * YS + (e - r * rl)] = src[e];
+      }
+    }
   }
   __syncthreads();
   if (u >= K) return;
@@ -262,12 +294,32 @@ __global__ void __launch_bounds__(128)
   // linear part: conj(Theta_u) . y  (Theta = theta[:M] + i theta[M:])
   const T* th = theta + ((long long)f * K + u) * 2 * M;
   T lr = T(0), li = T(0);
+  if (M == MT) {                                   // the common case: static indices,
+    T tv[2 * MT];                                  // theta in 16-byte loads
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
-  for (int k = 0; k < MT; ++k) {
-    if (k < M) {
-      const T tr = th[k], ti = th[M + k];
+      for (int q = 0; q < MT / 2; ++q) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(th) + q);
+        tv[4 * q] = a.x; tv[4 * q + 1] = a.y; tv[4 * q + 2] = a.z; tv[4 * q + 3] = a.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < MT; ++q) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(th) + q);
+        tv[2 * q] = a.x; tv[2 * q + 1] = a.y;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+      const T tr = tv[k], ti = tv[MT + k];
       lr = fma(tr, y[2 * k], fma(ti, y[2 * k + 1], lr));
       li = fma(tr, y[2 * k + 1], fma(-ti, y[2 * k], li));
+    }
+  } else {
+    for (int k = 0; k < M; ++k) {
+      const T tr = th[k], ti = th[M + k];
+      lr = fma(tr, ys[lane * YS + 2 * k], fma(ti, ys[lane * YS + 2 * k + 1], lr));
+      li = fma(tr, ys[lane * YS + 2 * k + 1], fma(-ti, ys[lane * YS + 2 * k], li));
     }
   }
   T gr = T(0), gi = T(0);
@@ -383,8 +435,9 @@ int launch_finish(const T* rx, long long rx_stride, int F, int K, int n_train, i
                   int n_points, const unsigned char* tx, const unsigned* live, T* est,
                   unsigned char* labels, unsigned long long* be, unsigned long long* se,
                   cudaStream_t s) {
-  dim3 block(32, 4);
-  dim3 grid((n_data + 31) / 32, (K + 3) / 4, F);
+  const int ku = MT <= 16 && sizeof(T) == 4 ? (K < 8 ? K : 8) : 4;   // users per CTA
+  dim3 block(32, ku);
+  dim3 grid((n_data + 31) / 32, (K + ku - 1) / ku, F);
   detect_finish_kernel<T, MT><<<grid, block, 0, s>>>(
       rx, rx_stride, K, n_train, n_data, M, coeff, theta, (T)p.w_g,
       (T)(1.0 / (2.0 * p.sigma_sq)), points, n_points, tx, live, est, labels, be, se);
