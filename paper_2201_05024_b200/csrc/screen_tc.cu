@@ -30,6 +30,9 @@
 //     test each (pilot, symbol) pair and ballot the results into the live-bit
 //     words (bit = pilot, word per symbol) -- the word layout of screen.cu;
 //   * the live words and the compact per-symbol lists go out as in screen.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kapsm_common.cuh"
 
 namespace kapsm {
@@ -80,6 +83,22 @@ KAPSM_DEV void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
 }
 KAPSM_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// TMA: one 3-D tile {32 floats, 128 rows, 1 frame} of the pilot rows into a
+// 128-byte-swizzled shared buffer (the UMMA K-major SW128 layout), completing
+// on an mbarrier
+KAPSM_DEV void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
+                           unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
+}
+KAPSM_DEV void mbar_arrive_tx(unsigned mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+
 KAPSM_DEV void sts_f4(unsigned a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
@@ -112,7 +131,7 @@ struct TcSmem {
   static constexpr int OFF_A = B_BYTES;                  // two buffers
   static constexpr int OFF_BITS = OFF_A + 2 * A_BYTES;
   static size_t bytes(int NW) {
-    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 64;
+    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 96;
   }
 };
 
@@ -121,7 +140,8 @@ __global__ void __launch_bounds__(TC_THREADS)
     detect_screen_tc_kernel(const float* __restrict__ rx, long long rx_stride, int n_train,
                             int n_data, int y_row0, int list_max_off, int M, float inv2s,
                             float dead, unsigned* __restrict__ live, int* __restrict__ cnt,
-                            float4* __restrict__ vals) {
+                            float4* __restrict__ vals, const __grid_constant__ CUtensorMap tmap,
+                            int use_tma) {
   using L = TcSmem<NT, KC>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned base for the swizzle atoms
@@ -132,7 +152,8 @@ __global__ void __launch_bounds__(TC_THREADS)
   unsigned* bits = reinterpret_cast<unsigned*>(base + L::OFF_BITS);        // [NW][NT]
   float* nyb = reinterpret_cast<float*>(base + L::OFF_BITS + (size_t)NW * NT * 4);
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nyb + NT);
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(mbar + 1);
+  unsigned long long* tbar = mbar + 1;                     // [2] TMA arrivals per A buffer
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(mbar + 3);
   const unsigned sB = base_s + L::OFF_B, sA = base_s + L::OFF_A;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -145,6 +166,8 @@ __global__ void __launch_bounds__(TC_THREADS)
 
   if (tid == 0) {
     mbar_init(mbar, 1);
+    mbar_init(tbar, 1);
+    mbar_init(tbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -168,6 +191,16 @@ __global__ void __launch_bounds__(TC_THREADS)
   auto load_a = [&](int mt, int b) {
     const int p0 = mt * TC_MROWS;
     const unsigned sa = sA + (unsigned)b * L::A_BYTES;
+    if (use_tma) {                          // one thread: KC boxes of 128 rows x 128 bytes
+      if (tid == 0) {
+        const unsigned bar = smem_u32(tbar + b);
+        mbar_arrive_tx(bar, (unsigned)(KC * TC_MROWS * 128));
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc)
+          tma_load_3d(sa + (unsigned)kc * TC_MROWS * 128, &tmap, 32 * kc, p0, f, bar);
+      }
+      return;
+    }
     for (int e = tid; e < TC_MROWS * KC * 8; e += TC_THREADS) {
       const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
       const int p = p0 + r;
@@ -214,8 +247,13 @@ __global__ void __launch_bounds__(TC_THREADS)
   const int col0 = (warp >> 2) * (NT / 2);
 
   for (int mt = 0; mt < n_mt; ++mt) {
-    cp_async_wait<0>();
-    fence_async_smem();
+    if (use_tma) {
+      while (!mbar_try_wait(tbar + (mt & 1), (unsigned)((mt >> 1) & 1))) {
+      }
+    } else {
+      cp_async_wait<0>();
+      fence_async_smem();
+    }
     __syncthreads();                        // A[mt] visible; previous epilogue done with TMEM
     if (tid == 0) {
       tc_fence_after();
@@ -341,6 +379,35 @@ __global__ void __launch_bounds__(TC_THREADS)
   }
 }
 
+// The 3-D tensor map {2M floats, rows per frame, frames} of rx for TMA loads of
+// pilot tiles (box {32 floats, 128 rows, 1}, 128-byte swizzle); 0 when the
+// layout does not allow it (rows not 16-byte multiples) -- the kernel then
+// stages the tiles with cp.async.
+static int make_pilot_map(CUtensorMap* map, const float* rx, long long rx_stride, int F, int M) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  memset(map, 0, sizeof(*map));
+  const long long D = 2LL * M;
+  if (!encode || D % 4 || rx_stride % D || rx_stride % 4 || ((size_t)rx & 15)) return 0;
+  const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)(rx_stride / D), (cuuint64_t)F};
+  const cuuint64_t strides[2] = {(cuuint64_t)D * 4, (cuuint64_t)rx_stride * 4};
+  const cuuint32_t box[3] = {32, (cuuint32_t)TC_MROWS, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(rx), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
 template <int NT, int KC>
 static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_train, int n_data,
                             int y_row0, int list_max_off, int M, kapsm_kernel_params p,
@@ -356,8 +423,11 @@ static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_t
       cudaSuccess)
     return KAPSM_ERR_CUDA;
   dim3 grid((n_data + NT - 1) / NT, F);
+  CUtensorMap tmap;
+  const int use_tma = make_pilot_map(&tmap, rx, rx_stride, F, M);
   kern<<<grid, TC_THREADS, smem, s>>>(rx, rx_stride, n_train, n_data, y_row0, list_max_off, M,
-                                      (float)(1.0 / (2.0 * p.sigma_sq)), 88.0f, live, cnt, vals);
+                                      (float)(1.0 / (2.0 * p.sigma_sq)), 88.0f, live, cnt, vals,
+                                      tmap, use_tma);
   return status_from(cudaGetLastError());
 }
 
