@@ -755,6 +755,20 @@ def main():
                           "reference code path)"),
                "bit_errors": r["bit_errors"]}
 
+    # ---------------- the reference harness's rows (kapsm bench) on the B200 ----------------
+    # bench_detection (pkg/src/kapsm/bench.py:108-201 schema, CSV_COLUMNS) at the
+    # acceptance suite's ladder cell (10,000 atoms x 4,096 inputs, 16 antennas,
+    # test_acceptance.py:318-330), checksum gate first, FP64 and FP32 templates
+    harness = None
+    if rank == 0 and world == 1:
+        harness = {}
+        for prec in ("f64", "f32"):
+            rep = K.bench_detection([10_000], [4_096], stages=("baseline", "tiled", "balanced"),
+                                    workers=(1,), repeats=5, seed=0, antennas=16,
+                                    engine_template=K.EngineConfig(precision=prec))
+            harness[prec] = json.loads(K.report_to_json(rep))["rows"]   # failed timings -> null
+            harness[prec + "_has_failures"] = rep.has_failures
+
     # ---------------- the other BASELINE configs (rank 0, N = 1) ----------------
     others = None
     if rank == 0 and world == 1 and not args.no_configs:
@@ -791,6 +805,7 @@ def main():
                               "compute / D2H overlapped across steps"),
                       "bit_errors_last_step": e2e_bit_err},
               "e2e_live_generation": live,
+              "kapsm_bench_rows": harness,
               "fp64": fp64,
               "other_configs": others,
               "correctness_gate": gate,
