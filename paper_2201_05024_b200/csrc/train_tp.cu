@@ -44,24 +44,26 @@ constexpr int TP_KS = 36;                // row stride of the ring's K matrix: 1
 constexpr int TP_SPAN = 28;              // P + W (< 32: slack for the live-term loads)
 __host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // takeover lead P
 
-// per-warp shared memory; the stage of step n = m - P holds the prefetched
-// inputs of that step: the pilot row of the sample taken over (m) and of the
-// sample leaving the window (m - TP_SPAN + 1), XR floats each, then the band
-// row (32), the live-list row (8 float4), the target and the live count
-__host__ __device__ constexpr int tp_xr(int D) { return (D + 3) & ~3; }
-__host__ __device__ constexpr int tp_sstr(int D) { return 2 * tp_xr(D) + 68; }
-struct TpSmem {
-  int ks, dsm, stg, qs, total;
-  __host__ __device__ TpSmem(int D, int W) {
-    int o = 0;
-    auto take = [&](int bytes) { int r = o; o = (o + bytes + 15) & ~15; return r; };
-    ks = take(TP_RING * TP_KS * 4);
-    dsm = take(TP_RING * 4);
-    stg = take(TP_STG * tp_sstr(D) * 4);
-    qs = take(2 * W * 4);
-    total = (o + 127) & ~127;
-  }
+// per-warp shared memory, a compile-time layout for DPL components per lane
+// (rows of up to 32 DPL floats); the stage of step n = m - P holds the
+// prefetched inputs of that step: the pilot row of the sample taken over (m)
+// and of the sample leaving the window (m - TP_SPAN + 1), XR floats each, then
+// the band row (32), the live-list row (8 float4), the target and the live count
+template <int DPL>
+struct TpL {
+  static constexpr int XR = 32 * DPL;
+  static constexpr int SSTR = 2 * XR + 68;                  // floats per stage
+  static constexpr int OKB = 2 * XR, OLV = OKB + 32, OB = OLV + 32, OLC = OB + 1;
+  static constexpr int KS = 0;                              // [32][TP_KS] K over ring pairs
+  static constexpr int DSM = KS + TP_RING * TP_KS * 4;      // [32] deltas
+  static constexpr int QS = DSM + TP_RING * 4;              // [32][2] (q_mid, q_last)
+  static constexpr int STG = QS + 64 * 4;                   // [STG][SSTR] stages
+  static constexpr int TOTAL = (STG + TP_STG * SSTR * 4 + 127) & ~127;
 };
+__host__ __device__ constexpr int tp_dpl(int M) { return (2 * M + 31) / 32; }
+__host__ __device__ constexpr int tp_total(int M) {
+  return tp_dpl(M) == 1 ? TpL<1>::TOTAL : tp_dpl(M) == 2 ? TpL<2>::TOTAL : TpL<4>::TOTAL;
+}
 
 KAPSM_DEV void cpa16(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -182,19 +184,19 @@ __global__ void __launch_bounds__(128, 6)
                          int* __restrict__ fs_out, float* __restrict__ theta_out,
                          int* __restrict__ nact_out, int* __restrict__ status_out) {
   extern __shared__ __align__(128) unsigned char smem_tp[];
+  using L = TpL<DPL>;
   const int Np = 2 * n_train, D = 2 * M, P = tp_lead(W);
-  const TpSmem L(D, W);
   const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * wpc + warp;
   if (task >= F * K) return;                    // warps are independent: no CTA barrier below
-  unsigned char* base = smem_tp + (size_t)warp * L.total;
+  unsigned char* base = smem_tp + (size_t)warp * L::TOTAL;
   const unsigned sbase = smem_u32(base);
-  float* Ks = reinterpret_cast<float*>(base + L.ks);       // [32][TP_KS] K over ring pairs
-  float* dsm = reinterpret_cast<float*>(base + L.dsm);     // [32] the step's deltas
-  const float* Sg = reinterpret_cast<const float*>(base + L.stg);   // [STG][SSTR] stages
-  float* qs = reinterpret_cast<float*>(base + L.qs);       // [W][2] (q_mid, q_last)
-  const int XR = tp_xr(D), SSTR = tp_sstr(D);
-  const int OKB = 2 * XR, OLV = OKB + 32, OB = OLV + 32, OLC = OB + 1;   // stage offsets
+  float* Ks = reinterpret_cast<float*>(base + L::KS);      // [32][TP_KS] K over ring pairs
+  float* dsm = reinterpret_cast<float*>(base + L::DSM);    // [32] the step's deltas
+  const float* Sg = reinterpret_cast<const float*>(base + L::STG);  // [STG][SSTR] stages
+  float* qs = reinterpret_cast<float*>(base + L::QS);      // [W][2] (q_mid, q_last)
+  constexpr int XR = L::XR, SSTR = L::SSTR;
+  constexpr int OKB = L::OKB, OLV = L::OLV, OB = L::OB, OLC = L::OLC;   // stage offsets
   const int f = task / K;
   const float* X = rx + (long long)f * rx_stride;
   const float* Bt = targets + (long long)task * Np;
@@ -221,69 +223,77 @@ __global__ void __launch_bounds__(128, 6)
   // target and the row's live count.  Each lane owns up to two pieces for the
   // whole chain: global address g + m * gm + (m >> 1) * gt, shared address
   // s + (m mod STG) * SSTR * 4, size 16 or 4 bytes (0: none).
+  // prefetch pieces into stage m mod STG (one cp.async group per step): the
+  // pilot rows of sample m and of the leaving sample m - SPAN + 1 (16-byte
+  // pieces, or 4-byte ones when rows are not 16-byte aligned), the band row
+  // and the live-list row (8 pieces each), the target and the row's live
+  // count.  A lane owns up to 3 pieces for the whole chain; each keeps a
+  // running global pointer for its sample mm (m or m - SPAN + 1):
+  // g + mm * gm + (mm >> 1) * gt, advanced by gm + (mm odd) gt per step.
   const int XP = vec ? D / 4 : D, NPC = 2 * XP + 18;
-  const unsigned sg_s = sbase + L.stg;
-  const char* pg[3];
+  const unsigned sg_s = sbase + L::STG;
+  const char* pp[3];
   long long pgm[3], pgt[3];
   unsigned ps[3];
-  int psz[3], plv[3];            // plv: 1 = the leaving sample's row (row index m - SPAN + 1)
+  int psz[3], poff[3];           // poff: the piece's sample is m - poff
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     int pc = lane + 32 * r;
-    pg[r] = nullptr; pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; plv[r] = 0;
+    const char* g = nullptr;
+    pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; poff[r] = 0;
     if (pc < 2 * XP) {
       const int lv = pc >= XP;
       if (lv) pc -= XP;
-      pg[r] = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
+      g = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
       pgt[r] = (long long)D * 4;
       ps[r] = sg_s + (unsigned)(lv * XR + (vec ? 4 * pc : pc)) * 4;
       psz[r] = vec ? 16 : 4;
-      plv[r] = lv;
+      poff[r] = lv ? TP_SPAN - 1 : 0;
     } else if (pc < 2 * XP + 8) {
       const int q = pc - 2 * XP;
-      pg[r] = reinterpret_cast<const char*>(KB + 4 * q);
+      g = reinterpret_cast<const char*>(KB + 4 * q);
       pgm[r] = 128;
       ps[r] = sg_s + (unsigned)(OKB + 4 * q) * 4;
       psz[r] = 16;
     } else if (pc < 2 * XP + 16) {
       const int q = pc - 2 * XP - 8;
-      pg[r] = reinterpret_cast<const char*>(LV + q);
+      g = reinterpret_cast<const char*>(LV + q);
       pgt[r] = (long long)TP_CAP * 16;
       ps[r] = sg_s + (unsigned)(OLV + 4 * q) * 4;
       psz[r] = gauss ? 16 : 0;
     } else if (pc == 2 * XP + 16) {
-      pg[r] = reinterpret_cast<const char*>(Bt);
+      g = reinterpret_cast<const char*>(Bt);
       pgm[r] = 4;
       ps[r] = sg_s + (unsigned)OB * 4;
       psz[r] = 4;
     } else if (pc == 2 * XP + 17) {
-      pg[r] = reinterpret_cast<const char*>(LC);
+      g = reinterpret_cast<const char*>(LC);
       pgt[r] = 4;
       ps[r] = sg_s + (unsigned)OLC * 4;
       psz[r] = gauss ? 4 : 0;
     }
+    // pointer for the piece of prefetch(0): sample -poff (may be negative: never issued)
+    const long long mm0 = -poff[r];
+    pp[r] = g ? g + mm0 * pgm[r] + (mm0 >> 1) * pgt[r] : nullptr;
   }
   const int nr = (NPC + 31) / 32;
-  // stage of step m - P: sample m's pieces while m < Np, the leaving row
-  // (sample m - SPAN + 1) while that exists.  Each role's global address is
-  // g + mm * gm + (mm >> 1) * gt for its sample mm.
-  auto prefetch = [&](int m) {
-    const int ml = m - TP_SPAN + 1;
-    const unsigned so = (unsigned)((m & (TP_STG - 1)) * SSTR) * 4;
+  int pm = 0;                    // the sample index m of the next prefetch
+  auto prefetch = [&]() {        // stage of sample pm (steps are prefetched in order)
+    const unsigned so = (unsigned)((pm & (TP_STG - 1)) * SSTR) * 4;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       if (r < nr) {
-        const int mm = plv[r] ? ml : m;
+        const int mm = pm - poff[r];
         const bool go = (unsigned)mm < (unsigned)Np;
-        const int mc = go ? mm : 0;
-        const char* g = pg[r] + mc * pgm[r] + (long long)(mc >> 1) * pgt[r];
-        cpa16_if(go && psz[r] == 16, ps[r] + so, g);
-        cpa4_if(go && psz[r] == 4, ps[r] + so, g);
+        cpa16_if(go && psz[r] == 16, ps[r] + so, pp[r]);
+        cpa4_if(go && psz[r] == 4, ps[r] + so, pp[r]);
+        pp[r] += pgm[r] + ((mm & 1) ? pgt[r] : 0);          // -> sample mm + 1
       }
     }
+    ++pm;
   };
   for (int i = 0; i < TP_AHEAD; ++i) {
-    prefetch(i);
+    prefetch();
     cp_async_commit();
   }
 
@@ -368,13 +378,13 @@ __global__ void __launch_bounds__(128, 6)
       c = mine ? 0.f : c;
       fs = mine ? -1 : fs;
       status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;   // kappa(r, r) = K[m][m]
-      const float rv = __frcp_rn(v);
+      const float rv = __fdividef(1.f, v);     // MUFU (the FP32 path's tolerance is 1e-4)
       idn = mine ? (v > 0.f ? rv : 0.f) : idn;
       bl = mine ? b - eps : bl;
       bh = mine ? b + eps : bh;
     }
     __syncwarp();                               // stage reads done before it is refilled
-    prefetch(m + TP_AHEAD);
+    prefetch();                                 // sample m + TP_AHEAD
     cp_async_commit();
     if (n < 0) continue;
     // ---- step n: the window's deltas, then the window update ----
@@ -389,8 +399,8 @@ __global__ void __launch_bounds__(128, 6)
     dsm[lane] = dl;
     __syncwarp();                               // deltas and the takeover's K row/column
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    const unsigned krow = sbase + L.ks + (unsigned)(lane * TP_KS) * 4;   // K[.][my sample]
-    const unsigned dsa = sbase + L.dsm;
+    const unsigned krow = sbase + L::KS + (unsigned)(lane * TP_KS) * 4;   // K[.][my sample]
+    const unsigned dsa = sbase + L::DSM;
 #pragma unroll
     for (int s = 0; s < 32; s += 4) {
       const float4 dd = lds_f4(dsa + 4u * s);
@@ -484,7 +494,7 @@ bool train_tp_supported(int n_train, int M, int W) {
   // the live terms of a sample are added TP_AHEAD steps after its takeover, which
   // must precede its entry into the window: P = TP_SPAN - W > TP_AHEAD
   if (W < 1 || tp_lead(W) <= TP_AHEAD || M < 1 || M > 64 || n_train < 1) return false;
-  return TpSmem(2 * M, W).total <= 200 * 1024;
+  return tp_total(M) <= 200 * 1024;
 }
 
 // stages (bit mask, all by default): 1 band rows, 2 pilot screen, 4 trainer --
@@ -518,15 +528,14 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
     if (r) return r;
   }
   if (!(stages & 4)) return KAPSM_OK;
-  const TpSmem L(2 * M, W);
   const int tasks = F * K;
   // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
   // so no other CTA (the concurrent detection screen) shares its SM;
   // throughput: 4 chains per CTA (several CTAs per SM)
   const bool lat = tasks <= tp_num_sms();
   int wpc = lat ? 1 : 4;
-  while (wpc > 1 && (size_t)L.total * wpc > 227 * 1024) wpc >>= 1;
-  size_t smem = (size_t)L.total * wpc;
+  while (wpc > 1 && (size_t)tp_total(M) * wpc > 227 * 1024) wpc >>= 1;
+  size_t smem = (size_t)tp_total(M) * wpc;
   if (lat && smem < 120 * 1024) smem = 120 * 1024;
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
   const int DPL = (2 * M + 31) / 32;
