@@ -131,7 +131,7 @@ struct TcSmem {
   static constexpr int OFF_A = B_BYTES;                  // two buffers
   static constexpr int OFF_BITS = OFF_A + 2 * A_BYTES;
   static size_t bytes(int NW) {
-    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 96;
+    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 96 + TC_MROWS * 4;
   }
 };
 
@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(TC_THREADS)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nyb + NT);
   unsigned long long* tbar = mbar + 1;                     // [2] TMA arrivals per A buffer
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(mbar + 3);
+  float* ath = reinterpret_cast<float*>(mbar + 4);          // [128] pilot thresholds of a tile
   const unsigned sB = base_s + L::OFF_B, sA = base_s + L::OFF_A;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -237,12 +238,103 @@ __global__ void __launch_bounds__(TC_THREADS)
     nyb[r] = shrink * s;
   }
 
+  const float half_t0 = 0.5f * dead / inv2s;
+  const int q = warp & 3;                   // TMEM lane quarter of this warp
+  if constexpr (NT == 128) {
+    // ---- transposed form: MMA M = 128 payload symbols (A = their rows, then
+    //      their rotations), N = 128 pilots (B = the pilot tile) -> TMEM lane =
+    //      symbol, column = pilot: Re c in columns 0..127, Im c in 128..255.
+    //      A thread tests its symbol against 32 pilots per TMEM load with one
+    //      OR-accumulated compare per pair; the live word is assembled only in
+    //      the rare chunks that have a live pair. ----
+    const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(128 >> 3) << 17) |
+                           ((unsigned)(128 >> 4) << 24);
+    const int sym = 32 * q + lane;                                 // this thread's symbol
+    float bsym = 0.f;                                              // (read after a barrier)
+    const int ph = (warp >> 2) * 64;                               // its half of the pilots
+    for (int mt = 0; mt < n_mt; ++mt) {
+      if (use_tma) {
+        while (!mbar_try_wait(tbar + (mt & 1), (unsigned)((mt >> 1) & 1))) {
+        }
+      } else {
+        cp_async_wait<0>();
+        fence_async_smem();
+      }
+      __syncthreads();                      // pilot tile visible; previous epilogue done
+      if (mt == 0) bsym = nyb[sym];
+      const unsigned sa = sA + (unsigned)(mt & 1) * L::A_BYTES;
+      if (tid == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {       // Re (payload rows), Im (rotated rows)
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const unsigned long long a =
+                  umma_desc_sw128(sB + kc * (2 * NT) * 128 + h * NT * 128 + ks * 32);
+              const unsigned long long b = umma_desc_sw128(sa + kc * TC_MROWS * 128 + ks * 32);
+              umma_tf32(tmem + 128 * h, a, b, idesc, (kc | ks) ? 1u : 0u);
+            }
+        }
+        umma_commit(smem_u32(mbar));
+      }
+      // pilot thresholds of this tile while the MMAs run (the buffer of the next
+      // tile was read by the previous MMA, complete by now)
+      if (tid < TC_MROWS) {
+        const int p = mt * TC_MROWS + tid;
+        float sx = 0.f;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = lds_f4(sa + (unsigned)kc * TC_MROWS * 128 + sw128_off(tid, j));
+            sx = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, sx))));
+          }
+        // live <=> max(Re c, |Im c|) > shrink (nx + ny) - T0 / 2
+        ath[tid] = p < n_train ? fmaf(shrink, sx, -half_t0) : __int_as_float(0x7f800000);
+      }
+      if (mt + 1 < n_mt) load_a(mt + 1, (mt + 1) & 1);
+      __syncthreads();                      // thresholds visible
+      while (!mbar_try_wait(mbar, (unsigned)(mt & 1))) {
+      }
+      tc_fence_after();
+      const unsigned lane_sel = (unsigned)(32 * q) << 16;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int pb = ph + 32 * c;                                // tile column = pilot
+        unsigned re[32], im[32];
+        tmem_ld32(tmem + lane_sel + (unsigned)pb, re);
+        tmem_ld32(tmem + lane_sel + (unsigned)(128 + pb), im);
+        float4 th4[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) th4[k] = lds_f4(smem_u32(ath + pb + 4 * k));
+        tmem_wait_ld();
+        const float* thp = reinterpret_cast<const float*>(th4);
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
+          any |= m > thp[j] + bsym;
+        }
+        unsigned w = 0;
+        if (any) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
+            w |= (m > thp[j] + bsym ? 1u : 0u) << j;
+          }
+        }
+        const int wrd = (mt * TC_MROWS + pb) >> 5;
+        if (wrd < NW) bits[wrd * NT + sym] = w;
+      }
+      tc_fence_before();
+    }
+  } else {
   // instruction descriptor: F32 accumulate, TF32 A and B, both K-major,
   // N = 2 NT (bits 17-22, >> 3), M = 128 (bits 24-28, >> 4)
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(2 * NT >> 3) << 17) |
                          ((unsigned)(TC_MROWS >> 4) << 24);
-  const float half_t0 = 0.5f * dead / inv2s;
-  const int q = warp & 3;                   // TMEM lane quarter = pilots 32q .. 32q + 31
   constexpr int CH = NT / 64;               // 32-symbol column chunks per warp
   const int col0 = (warp >> 2) * (NT / 2);
 
@@ -308,6 +400,7 @@ __global__ void __launch_bounds__(TC_THREADS)
       if (wrd < NW) bits[wrd * NT + cb + lane] = mine;
     }
     tc_fence_before();
+  }
   }
   __syncthreads();
   if (warp == 0)
