@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(TC_THREADS)
           any |= m > thp[j] + bsym;
         }
         unsigned w = 0;
-        if (any) {
+        if (__builtin_expect(any, false)) {   // rare: keep it a branch, not predicated code
+          asm volatile("" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
