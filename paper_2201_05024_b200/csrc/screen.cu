@@ -435,7 +435,10 @@ int launch_finish(const T* rx, long long rx_stride, int F, int K, int n_train, i
                   int n_points, const unsigned char* tx, const unsigned* live, T* est,
                   unsigned char* labels, unsigned long long* be, unsigned long long* se,
                   cudaStream_t s) {
-  const int ku = MT <= 16 && sizeof(T) == 4 ? (K < 8 ? K : 8) : 4;   // users per CTA
+  // users per CTA: all of a frame's (up to 8) for batches of frames -- the
+  // payload rows staged once; 4 for a few frames, where more, smaller CTAs
+  // shorten the single-frame latency
+  const int ku = (MT <= 16 && sizeof(T) == 4 && F >= 8) ? (K < 8 ? K : 8) : 4;
   dim3 block(32, ku);
   dim3 grid((n_data + 31) / 32, (K + ku - 1) / ku, F);
   detect_finish_kernel<T, MT><<<grid, block, 0, s>>>(
