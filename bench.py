@@ -474,7 +474,7 @@ def main():
         rxs = T * M_ANT * 2
         fns = {}
         if batch_path:
-            nb = int(lib.kapsm_internal_train_tp_ws_bytes(F, N_TRAIN))
+            nb = int(lib.kapsm_internal_train_tp_ws_bytes(F, N_TRAIN, c.window))
             ws = torch.empty(((nb + 15) // 16 * 4,), dtype=torch.int32, device=dev)
 
             def tp(stage):

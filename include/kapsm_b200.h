@@ -242,10 +242,12 @@ int kapsm_count_mismatch(const void* a, const void* b, long long n, int elem_byt
  * gram_ws: workspace of kapsm_pipeline_workspace_bytes() bytes -- the pilot
  *          Gram F x (2*n_train) x ld, ld = 2*n_train + 16 rounded up to 32,
  *          followed by 32 x ld zero elements (the trainer's staged reads run
- *          past the last sample into them); in FP32 throughput mode (more
- *          chains than SMs, window <= 25, M <= 64) the band rows and pilot
- *          screen of the one-warp-per-chain trainer instead.  Other arguments as
- * for the three stages.  Captured into a CUDA graph by the host.
+ *          past the last sample into them); in FP32, when the
+ *          one-warp-per-chain trainer runs instead (M <= 64 and window <= 149,
+ *          with more chains than SMs, or with a window / pilot block beyond
+ *          the Gram trainer's fast schedule: window > 23, the C3 sweep, or
+ *          the C4 full band), its band rows and pilot screen.  Other
+ *          arguments as for the three stages.  Captured into a CUDA graph by the host.
  * ------------------------------------------------------------------------- */
 /* Bytes of gram_ws the pipelines need for this shape (elem_bytes 4: FP32,
  * 8: FP64); -1 on invalid arguments. */

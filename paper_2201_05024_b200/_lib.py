@@ -89,7 +89,7 @@ SIGNATURES = {
                                                         _I, _D, _KP, _P, _P, _I, _I, _P, _LL, _P,
                                                         _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                                         _P]),
-    "kapsm_internal_train_tp_ws_bytes": (_LL, [_I, _I]),
+    "kapsm_internal_train_tp_ws_bytes": (_LL, [_I, _I, _I]),
     "kapsm_internal_train_tp_f32": (_I, [_I, _P, _LL, _P, _I, _I, _I, _I, _I, _D, _KP, _P, _P, _P,
                                          _P, _P, _P, _P, _P]),
     "kapsm_internal_screen_simt_f32": (_I, [_P, _LL, _I, _I, _I, _I, _KP, _P, _P]),

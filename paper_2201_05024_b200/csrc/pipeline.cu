@@ -7,7 +7,9 @@
 
 namespace kapsm {
 bool train_tp_supported(int n_train, int M, int W);
-size_t train_tp_ws_bytes(int F, int n_train);
+template <typename T>
+bool train_takes_general(int Np, int W);
+size_t train_tp_ws_bytes(int F, int n_train, int W);
 int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
              int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
              void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
@@ -41,7 +43,8 @@ static bool use_tp(int F, int K, int n_train, int M, int window, long long ld,
     return false;
   } else {
     if (mode == TRAINER_GRAM || !kapsm::train_tp_supported(n_train, M, window)) return false;
-    return mode == TRAINER_TP || (long long)F * K > pipe_num_sms();
+    return mode == TRAINER_TP || (long long)F * K > pipe_num_sms() ||
+           kapsm::train_takes_general<float>(2 * n_train, window);
   }
 }
 
@@ -55,7 +58,7 @@ extern "C" long long kapsm_pipeline_workspace_bytes(int F, int K, int n_train, i
   const long long Np = 2LL * n_train, ld = (Np + 16 + 31) / 32 * 32;
   const long long gram = ((long long)F * Np + 32) * ld * elem_bytes;
   if (elem_bytes == 4 && use_tp<float>(F, K, n_train, M, window, ld))
-    return (long long)kapsm::train_tp_ws_bytes(F, n_train);
+    return (long long)kapsm::train_tp_ws_bytes(F, n_train, window);
   return gram;
 }
 

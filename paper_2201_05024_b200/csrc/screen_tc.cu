@@ -123,34 +123,41 @@ KAPSM_DEV float4 row_f4(const float* row, int q, int n, bool vec) {
   return v;
 }
 
-template <int NT, int KC>
+template <int NT, int KC, bool GB = false>
 struct TcSmem {
   static constexpr int B_BYTES = 2 * NT * 128 * KC;
   static constexpr int A_BYTES = TC_MROWS * 128 * KC;
   static constexpr int OFF_B = 0;
   static constexpr int OFF_A = B_BYTES;                  // two buffers
   static constexpr int OFF_BITS = OFF_A + 2 * A_BYTES;
+  // GB: the live words go straight to global memory (long pilot blocks,
+  // whose NW x NT words would not fit beside the tiles)
   static size_t bytes(int NW) {
-    return 1024 + (size_t)OFF_BITS + (size_t)NW * NT * 4 + NT * 4 + 96 + TC_MROWS * 4;
+    return 1024 + (size_t)OFF_BITS + (GB ? 0 : (size_t)NW * NT * 4) + NT * 4 + 96 + TC_MROWS * 4;
   }
 };
 
-template <int NT, int KC>
+template <int NT, int KC, bool GB>
 __global__ void __launch_bounds__(TC_THREADS)
     detect_screen_tc_kernel(const float* __restrict__ rx, long long rx_stride, int n_train,
                             int n_data, int y_row0, int list_max_off, int M, float inv2s,
                             float dead, unsigned* __restrict__ live, int* __restrict__ cnt,
                             float4* __restrict__ vals, const __grid_constant__ CUtensorMap tmap,
                             int use_tma) {
-  using L = TcSmem<NT, KC>;
+  using L = TcSmem<NT, KC, GB>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned base for the swizzle atoms
   const unsigned raw_s = smem_u32(smem_raw);
   const unsigned base_s = (raw_s + 1023u) & ~1023u;
   unsigned char* base = smem_raw + (base_s - raw_s);
   const int NW = (n_train + 31) / 32;
-  unsigned* bits = reinterpret_cast<unsigned*>(base + L::OFF_BITS);        // [NW][NT]
-  float* nyb = reinterpret_cast<float*>(base + L::OFF_BITS + (size_t)NW * NT * 4);
+  const int f = blockIdx.y, t0 = blockIdx.x * NT;
+  // live words [NW][NT] in shared memory, or (GB) in place in the output
+  // [NW][n_data] (word w of symbol t0 + s at bits[w * BST + s])
+  unsigned* lf = live + (long long)f * NW * n_data;
+  unsigned* bits = GB ? lf + t0 : reinterpret_cast<unsigned*>(base + L::OFF_BITS);
+  const long long BST = GB ? n_data : NT;
+  float* nyb = reinterpret_cast<float*>(base + L::OFF_BITS + (GB ? 0 : (size_t)NW * NT * 4));
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nyb + NT);
   unsigned long long* tbar = mbar + 1;                     // [2] TMA arrivals per A buffer
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(mbar + 3);
@@ -158,7 +165,6 @@ __global__ void __launch_bounds__(TC_THREADS)
   const unsigned sB = base_s + L::OFF_B, sA = base_s + L::OFF_A;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int f = blockIdx.y, t0 = blockIdx.x * NT;
   const int D = 2 * M;
   const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
   const float* Xf = rx + (long long)f * rx_stride;
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS)
           }
         }
         const int wrd = (mt * TC_MROWS + pb) >> 5;
-        if (wrd < NW) bits[wrd * NT + sym] = w;
+        if (wrd < NW && (!GB || t0 + sym < n_data)) bits[wrd * BST + sym] = w;
       }
       tc_fence_before();
     }
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(TC_THREADS)
         const unsigned bj = __ballot_sync(0xffffffffu, m > a_thr + nyb[cb + j]);
         mine = lane == j ? bj : mine;
       }
-      if (wrd < NW) bits[wrd * NT + cb + lane] = mine;
+      if (wrd < NW && (!GB || t0 + cb + lane < n_data)) bits[wrd * BST + cb + lane] = mine;
     }
     tc_fence_before();
   }
@@ -409,10 +415,11 @@ __global__ void __launch_bounds__(TC_THREADS)
                  : "memory");
 
   // ---- live words out (word-major, coalesced over the symbols) ----
-  unsigned* lf = live + (long long)f * NW * n_data;
-  for (int i = tid; i < NW * NT; i += TC_THREADS) {
-    const int w = i / NT, tt = t0 + (i - w * NT);
-    if (tt < n_data) lf[(long long)w * n_data + tt] = bits[i];
+  if (!GB) {
+    for (int i = tid; i < NW * NT; i += TC_THREADS) {
+      const int w = i / NT, tt = t0 + (i - w * NT);
+      if (tt < n_data) lf[(long long)w * n_data + tt] = bits[i];
+    }
   }
   // ---- compact list of each symbol's live pilots in pilot order (those
   //      with p <= t + list_max_off), kernel values from explicit differences
@@ -427,7 +434,7 @@ __global__ void __launch_bounds__(TC_THREADS)
     if (t < n_data) {
       const int pmax = t + list_max_off;
       for (int w = 0; w < NW && w * 32 <= pmax; ++w) {
-        unsigned b = bits[w * NT + r];
+        unsigned b = bits[w * BST + r];
         while (b) {
           const int pp = w * 32 + __ffs(b) - 1;
           b &= b - 1;
@@ -507,12 +514,13 @@ static int launch_screen_tc(const float* rx, long long rx_stride, int F, int n_t
                             int y_row0, int list_max_off, int M, kapsm_kernel_params p,
                             unsigned* live, int* cnt, float4* vals, cudaStream_t s) {
   const int NW = (n_train + 31) / 32;
-  size_t smem = TcSmem<NT, KC>::bytes(NW);
+  const bool gb = TcSmem<NT, KC>::bytes(NW) > 227 * 1024;   // long pilot blocks (C4 full band)
+  size_t smem = gb ? TcSmem<NT, KC, true>::bytes(NW) : TcSmem<NT, KC>::bytes(NW);
   // at least 112 KB: never co-resident with a latency-mode trainer CTA (120 KB),
   // so the concurrent screen does not slow a critical warp down (screen.cu)
   if (smem < 112 * 1024) smem = 112 * 1024;
   if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
-  auto kern = detect_screen_tc_kernel<NT, KC>;
+  auto kern = gb ? detect_screen_tc_kernel<NT, KC, true> : detect_screen_tc_kernel<NT, KC, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return KAPSM_ERR_CUDA;

@@ -1017,6 +1017,18 @@ int train(const T* gram, long long ld, long long gram_stride, const T* rx, long 
                                    theta0, coeff, first_step, theta, n_active, status, dbg);
 }
 
+// true when train<T> leaves its fast schedule at this shape: the general
+// trainer, or the latency schedule with its targets staged beside the Gram
+// columns (long pilot blocks); the FP32 pipeline prefers the one-warp
+// trainer there (pipeline.cu)
+template <typename T>
+bool train_takes_general(int Np, int W) {
+  return W > TC_MAX_W || Np > TC_MAX_NP || GroupSmem<T, 1, 2>(W, Np, true).total > 227 * 1024 ||
+         GroupSmem<T, 1, 2>(W, Np, false).total > 227 * 1024;
+}
+template bool train_takes_general<float>(int, int);
+template bool train_takes_general<double>(int, int);
+
 }  // namespace kapsm
 
 extern "C" int kapsm_max_window(void) { return kapsm::train_wide_max_window(); }

@@ -95,28 +95,29 @@ KAPSM_DEV void stg_if<int>(bool p, int* dst, int v) {
                ::"l"(dst), "r"(v), "r"((int)p) : "memory");
 }
 
-// K[m][m-d] for d = 0..31 (0 where m - d < 0): the band of the realified
-// pilot Gram that a chain's ring can meet.  Realified sample m = 2t + beta is
+// K[m][m-d] for d = 0..R-1 (0 where m - d < 0): the band of the realified
+// pilot Gram that a chain's ring of R slots can meet (R = 32, or 32 NW for
+// the wide trainer below).  Realified sample m = 2t + beta is
 // r1(x_t) (beta = 0) or r2(x_t) (beta = 1) of pilot x_t (apsm.py:156-182).
-// One thread per complex pilot pair (t, t - dt), dt = 0..16: one pass over the
+// One thread per complex pilot pair (t, t - dt), dt = 0..R/2: one pass over the
 // antennas gives c = x^H y (y = x_t, x = x_{t-dt}) and the three distinct
 // distances |x - y|, |x + iy|, |x - iy| by explicit differences, hence the
 // 2 x 2 realified block: linear parts Re c, Im c, -Im c, Re c and Gaussian
 // parts of the matching distances (as screen.cu's list values).
 __global__ void __launch_bounds__(256)
     band_kernel(const float* __restrict__ rx, long long rx_stride, int n_train, int M, float w_l,
-                float w_g, float inv2s, float* __restrict__ kband) {
-  const int Np = 2 * n_train, D = 2 * M;
+                float w_g, float inv2s, float* __restrict__ kband, int R) {
+  const int Np = 2 * n_train, D = 2 * M, H = R / 2 + 1;
   const int f = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_train * 17) return;
-  const int t = i / 17, dt = i - t * 17, tp = t - dt;
-  float* kb = kband + (long long)f * Np * 32;
+  if (i >= n_train * H) return;
+  const int t = i / H, dt = i - t * H, tp = t - dt;
+  float* kb = kband + (long long)f * Np * R;
   if (tp < 0) {                                           // before the first sample: zeros
     for (int be = 0; be < 2; ++be)
       for (int al = 0; al < 2; ++al) {
         const int d = 2 * dt + be - al;
-        if (d >= 0 && d < 32) kb[(long long)(2 * t + be) * 32 + d] = 0.f;
+        if (d >= 0 && d < R) kb[(long long)(2 * t + be) * R + d] = 0.f;
       }
     return;
   }
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256)
   for (int be = 0; be < 2; ++be)
     for (int al = 0; al < 2; ++al) {
       const int d = 2 * dt + be - al;
-      if (d >= 0 && d < 32) kb[(long long)(2 * t + be) * 32 + d] = vals[al][be];
+      if (d >= 0 && d < R) kb[(long long)(2 * t + be) * R + d] = vals[al][be];
     }
 }
 
@@ -465,6 +466,394 @@ __global__ void __launch_bounds__(128, 6)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2w: the same restatement for windows beyond the one-warp ring (W > 21, the
+// C3 sweep): one CTA of NW warps per chain, thread j owns ring slot j of
+// R = 32 NW slots (P = R - 4 - W).  Per step, one CTA barrier:
+//   phase A  live terms of sample m - 2 (its owner warp), takeover of sample m
+//            (every thread writes its entry of K's new row / column; the owner
+//            warp forms f(r_m) from its theta replica, the previous step's
+//            coefficients and the band row), the prefetch of sample m + 6, and
+//            each slot's delta -> dsm[n & 1], coefficient -> csm[n & 1];
+//   barrier  (publishes K, deltas, coefficients and the next stage);
+//   phase B  Y_j += sum over the window's slots s of delta_s K[s][j] (16-byte
+//            rows of K, packed FP32x2 FMAs), then the leaving sample's
+//            coefficient is final: every warp adds c_a r_a to its theta replica.
+// Double-buffered deltas / coefficients make the one barrier sufficient.  The
+// step is bound by the shared-memory reads of the window update:
+// W x (W + P) x 4 bytes per step (128 B/clk per SM).
+constexpr int TPW_STG = 16;              // stages: read up to 2 steps back, 6 ahead
+constexpr int TPW_MAX_NW = 5;            // W <= 32 NW - 4 - TP_AHEAD - 1 = 149
+
+template <int DPL, int NW>
+struct TpwL {
+  static constexpr int R = 32 * NW, KS = R + 4, XR = 32 * DPL;
+  static constexpr int SSTR = 2 * XR + R + 36;              // floats per stage
+  static constexpr int OKB = 2 * XR, OLV = OKB + R, OB = OLV + 32, OLC = OB + 1;
+  static constexpr int KSO = 0;                             // [R][KS] K over ring pairs
+  static constexpr int DSM = KSO + R * KS * 4;              // [2][R] deltas
+  static constexpr int CSM = DSM + 2 * R * 4;               // [2][R] coefficients
+  static constexpr int QS = CSM + 2 * R * 4;                // [R][2] (q_mid, q_last)
+  static constexpr int RED = QS + 2 * R * 4;                // nact, status
+  static constexpr int STG = RED + 16;                      // [TPW_STG][SSTR] stages
+  static constexpr int TOTAL = (STG + TPW_STG * SSTR * 4 + 127) & ~127;
+};
+__host__ __device__ constexpr int tpw_nw(int W) {          // smallest ring with P > TP_AHEAD
+  return (W + 4 + TP_AHEAD + 1 + 31) / 32 < 2 ? 2 : (W + 4 + TP_AHEAD + 1 + 31) / 32;
+}
+template <int NW>
+__host__ __device__ constexpr int tpw_total(int M) {
+  return tp_dpl(M) == 1 ? TpwL<1, NW>::TOTAL
+                        : tp_dpl(M) == 2 ? TpwL<2, NW>::TOTAL : TpwL<4, NW>::TOTAL;
+}
+static int tpw_total_rt(int NW, int M) {
+  switch (NW) {
+    case 2: return tpw_total<2>(M);
+    case 3: return tpw_total<3>(M);
+    case 4: return tpw_total<4>(M);
+    default: return tpw_total<5>(M);
+  }
+}
+
+KAPSM_DEV float2 ffma2(float2 a, float2 b, float2 c) {     // packed FP32x2 FMA (FFMA2)
+  unsigned long long ra, rb, rc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rc) : "l"(ra), "l"(rb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(rc));
+  return r;
+}
+
+template <int DPL, int NW>
+__global__ void __launch_bounds__(32 * NW, 1)
+    apsm_train_tpw_kernel(const float* __restrict__ rx, long long rx_stride,
+                          const float* __restrict__ targets, const float* __restrict__ kband,
+                          const unsigned* __restrict__ plive, const int* __restrict__ pcnt,
+                          const float4* __restrict__ pvals, int F, int K, int n_train, int M,
+                          int W, float eps, float w_l, float w_g, float inv2s,
+                          const float* __restrict__ qtab, float* __restrict__ coeff_out,
+                          int* __restrict__ fs_out, float* __restrict__ theta_out,
+                          int* __restrict__ nact_out, int* __restrict__ status_out) {
+  extern __shared__ __align__(128) unsigned char smem_tp[];
+  using L = TpwL<DPL, NW>;
+  constexpr int R = L::R, KS = L::KS, NT = 32 * NW, XR = L::XR, SSTR = L::SSTR;
+  constexpr int OKB = L::OKB, OLV = L::OLV, OB = L::OB, OLC = L::OLC;
+  constexpr int SPAN = R - 4;
+  const int Np = 2 * n_train, D = 2 * M, P = SPAN - W;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, j = tid;   // j: my slot
+  const int task = blockIdx.x;
+  if (task >= F * K) return;
+  float* Ks = reinterpret_cast<float*>(smem_tp + L::KSO);
+  float* dsm = reinterpret_cast<float*>(smem_tp + L::DSM);
+  float* csm = reinterpret_cast<float*>(smem_tp + L::CSM);
+  float* qs = reinterpret_cast<float*>(smem_tp + L::QS);
+  int* red = reinterpret_cast<int*>(smem_tp + L::RED);
+  const float* Sg = reinterpret_cast<const float*>(smem_tp + L::STG);
+  const int f = task / K;
+  const float* X = rx + (long long)f * rx_stride;
+  const float* Bt = targets + (long long)task * Np;
+  const float* KB = kband + (long long)f * Np * R;
+  const int NWp = (n_train + 31) / 32;
+  const unsigned* LW = plive + (long long)f * NWp * n_train;
+  const int* LC = pcnt + (long long)f * n_train;
+  const float4* LV = pvals + (long long)f * n_train * TP_CAP;
+  float* Cout = coeff_out + (long long)task * Np;
+  int* FSout = fs_out + (long long)task * Np;
+  const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
+  const bool gauss = w_g != 0.f;
+
+  for (int i = tid; i < R * KS; i += NT) Ks[i] = 0.f;
+  for (int i = tid; i < 2 * R; i += NT) dsm[i] = csm[i] = 0.f;
+  for (int i = tid; i < W; i += NT) {
+    qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
+    qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
+  }
+  if (tid == 0) red[0] = red[1] = 0;
+
+  // prefetch pieces of step m's stage, spread over the CTA (<= 2 per thread):
+  // pilot rows of m and of the leaving sample m - SPAN + 1, the band row (R/4
+  // pieces), the live-list row (8), the target, the live count
+  const int XP = vec ? D / 4 : D, NPC = 2 * XP + R / 4 + 10;
+  const unsigned sg_s = smem_u32(smem_tp) + L::STG;
+  const char* pp[2];
+  long long pgm[2], pgt[2];
+  unsigned ps[2];
+  int psz[2], poff[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    int pc = tid + NT * r;
+    const char* g = nullptr;
+    pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; poff[r] = 0;
+    if (pc < 2 * XP) {
+      const int lv = pc >= XP;
+      if (lv) pc -= XP;
+      g = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
+      pgt[r] = (long long)D * 4;
+      ps[r] = sg_s + (unsigned)(lv * XR + (vec ? 4 * pc : pc)) * 4;
+      psz[r] = vec ? 16 : 4;
+      poff[r] = lv ? SPAN - 1 : 0;
+    } else if (pc < 2 * XP + R / 4) {
+      const int q = pc - 2 * XP;
+      g = reinterpret_cast<const char*>(KB + 4 * q);
+      pgm[r] = (long long)R * 4;
+      ps[r] = sg_s + (unsigned)(OKB + 4 * q) * 4;
+      psz[r] = 16;
+    } else if (pc < 2 * XP + R / 4 + 8) {
+      const int q = pc - 2 * XP - R / 4;
+      g = reinterpret_cast<const char*>(LV + q);
+      pgt[r] = (long long)TP_CAP * 16;
+      ps[r] = sg_s + (unsigned)(OLV + 4 * q) * 4;
+      psz[r] = gauss ? 16 : 0;
+    } else if (pc == 2 * XP + R / 4 + 8) {
+      g = reinterpret_cast<const char*>(Bt);
+      pgm[r] = 4;
+      ps[r] = sg_s + (unsigned)OB * 4;
+      psz[r] = 4;
+    } else if (pc == 2 * XP + R / 4 + 9) {
+      g = reinterpret_cast<const char*>(LC);
+      pgt[r] = 4;
+      ps[r] = sg_s + (unsigned)OLC * 4;
+      psz[r] = gauss ? 4 : 0;
+    }
+    const long long mm0 = -poff[r];
+    pp[r] = g ? g + mm0 * pgm[r] + (mm0 >> 1) * pgt[r] : nullptr;
+  }
+  const int nr = (NPC + NT - 1) / NT;
+  int pm = 0;
+  auto prefetch = [&]() {
+    const unsigned so = (unsigned)((pm & (TPW_STG - 1)) * SSTR) * 4;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r < nr) {
+        const int mm = pm - poff[r];
+        const bool go = (unsigned)mm < (unsigned)Np;
+        cpa16_if(go && psz[r] == 16, ps[r] + so, pp[r]);
+        cpa4_if(go && psz[r] == 4, ps[r] + so, pp[r]);
+        pp[r] += pgm[r] + ((mm & 1) ? pgt[r] : 0);
+      }
+    }
+    ++pm;
+  };
+  for (int i = 0; i < TP_AHEAD; ++i) {
+    prefetch();
+    cp_async_commit();
+  }
+  cp_async_wait<TP_AHEAD - 1>();
+  __syncthreads();
+
+  float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
+  int samp = -(1 << 30), fs = -1, nact = 0, status = 0;
+  float th[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) th[i] = 0.f;
+  int sm = 0;                                   // slot of m = (n + P) mod R
+  const unsigned krow = smem_u32(Ks) + (unsigned)(j * KS) * 4;   // K[.][my sample]
+
+  for (int n = -P; n < Np; ++n) {
+    const int m = n + P;
+    // ---- phase A: live Gaussian terms of sample ml = m - 2 (final, older c) ----
+    const int ml = m - TP_LIVE_LAG;
+    int sml = sm - TP_LIVE_LAG;
+    sml += sml < 0 ? R : 0;
+    if (gauss && ml >= 0 && ml < Np && warp == (sml >> 5)) {
+      const float* sl = Sg + (ml & (TPW_STG - 1)) * SSTR;
+      const int cnt = __float_as_int(sl[OLC]);
+      const int bt = ml & 1;
+      float part = 0.f;
+      if (cnt > 0) {
+        if (lane < 2 * cnt) {
+          const float4 v4 = reinterpret_cast<const float4*>(sl + OLV)[lane >> 1];
+          const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
+          if (a <= ml - SPAN) {
+            const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
+            part = w_g * __ldcg(Cout + a) * kap;
+          }
+        }
+      } else if (cnt < 0) {                     // more live pilots than the list holds
+        const int tl = ml >> 1;
+        const float* xm = X + (long long)tl * D;
+        for (int w = lane; w < NWp; w += 32) {
+          unsigned bits = LW[(long long)w * n_train + tl];
+          while (bits) {
+            const int p = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const float* xa = X + (long long)p * D;
+            for (int al = 0; al < 2; ++al) {
+              const int a = 2 * p + al;
+              if (a > ml - SPAN) continue;
+              float dist = 0.f;
+              for (int e = 0; e < D; ++e) {
+                const float z = rcomp(xa, e, al) - rcomp(xm, e, bt);
+                dist = fmaf(z, z, dist);
+              }
+              part = fmaf(w_g * __ldcg(Cout + a), exp_fast(-dist * inv2s), part);
+            }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, part != 0.f)) {
+        part = warp_sum_f(part);
+        if (j == sml) Y += part;
+      }
+    }
+    // ---- takeover of sample m into slot sm ----
+    const float* sg = Sg + (m & (TPW_STG - 1)) * SSTR;
+    if (m < Np) {
+      int d = sm - j;                           // m - (the sample in my slot)
+      d += d < 0 ? R : 0;
+      const float v = sg[OKB + d];
+      Ks[sm * KS + j] = v;                      // K is symmetric: row and column
+      Ks[j * KS + sm] = v;
+      if (warp == (sm >> 5)) {                  // the owner warp forms f_n(r_m)
+        const int bt = m & 1;
+        float pf = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          const int e = lane + 32 * i;
+          if (e < D) {
+            const float x0 = sg[e], x1 = sg[e ^ 1];
+            pf = fmaf(th[i], bt ? ((e & 1) ? -x1 : x1) : x0, pf);
+          }
+        }
+        pf *= w_l;
+        const float* cprev = csm + ((n - 1) & 1) * R;
+        for (int dd = P + 1 + lane; dd < P + W; dd += 32) {   // the window [n-W+1, n-1]
+          int s = sm - dd;
+          s += s < 0 ? R : 0;
+          pf = fmaf(cprev[s], sg[OKB + dd], pf);
+        }
+        const float init = warp_sum_f(pf);
+        if (j == sm) {
+          const float kd = sg[OKB], b = sg[OB];
+          samp = m;
+          Y = init;
+          c = 0.f;
+          fs = -1;
+          status |= !(kd > 0.f) ? (int)KAPSM_TRAIN_DEGENERATE : 0;   // kappa(r, r)
+          idn = kd > 0.f ? __fdividef(1.f, kd) : 0.f;
+          bl = b - eps;
+          bh = b + eps;
+        }
+      }
+    }
+    prefetch();                                 // sample m + TP_AHEAD
+    cp_async_commit();
+    const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
+    if (n >= 0) {                               // ---- step n: my slot's delta ----
+      const float qm = qs[2 * cj], ql = qs[2 * cj + 1];
+      const float q = samp == n ? ql : qm;
+      const bool inw = (unsigned)(samp - lo) <= (unsigned)cj;
+      float dl = q * idn * (fmaxf(bl - Y, 0.f) + fminf(bh - Y, 0.f));
+      dl = inw ? dl : 0.f;
+      c += dl;
+      fs = (dl != 0.f && fs < 0) ? n : fs;
+      dsm[(n & 1) * R + j] = dl;
+      csm[(n & 1) * R + j] = c;
+    }
+    cp_async_wait<TP_AHEAD - 1>();              // my pieces of sample m + 1 landed
+    __syncthreads();
+    if (n >= 0) {
+      // ---- phase B: Y_j += sum over the window's slots of delta_s K[s][j] ----
+      int sn = sm - P;
+      sn += sn < 0 ? R : 0;                     // slot of n
+      int slo = sn - cj;
+      slo += slo < 0 ? R : 0;                   // slot of lo
+      const int c0 = slo >> 2, nch = (n >> 2) - (lo >> 2) + 1;
+      const int e1 = c0 + nch < R / 4 ? c0 + nch : R / 4;
+      const float4* dd4 = reinterpret_cast<const float4*>(dsm + (n & 1) * R);
+      const float4* kk4 = reinterpret_cast<const float4*>(Ks + j * KS);
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+      int k = c0;
+#pragma unroll 2
+      for (; k + 1 < e1; k += 2) {
+        const float4 d0 = dd4[k], k0 = kk4[k], d1 = dd4[k + 1], k1 = kk4[k + 1];
+        a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+        a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+        a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+        a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+      }
+      if (k < e1) {
+        const float4 d0 = dd4[k], k0 = kk4[k];
+        a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+        a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+      }
+      const int rest = nch - (e1 - c0);         // wrapped part: chunks 0 .. rest-1
+      k = 0;
+#pragma unroll 2
+      for (; k + 1 < rest; k += 2) {
+        const float4 d0 = dd4[k], k0 = kk4[k], d1 = dd4[k + 1], k1 = kk4[k + 1];
+        a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+        a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+        a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+        a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+      }
+      if (k < rest) {
+        const float4 d0 = dd4[k], k0 = kk4[k];
+        a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+        a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+      }
+      Y += ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+      // ---- the sample leaving after this step: its coefficient is final ----
+      const int a = n - W + 1;                  // == m - SPAN + 1: its row is in the stage
+      if (a >= 0) {
+        int sa = sm - (SPAN - 1);
+        sa += sa < 0 ? R : 0;
+        const float ca = csm[(n & 1) * R + sa];
+        const int ba = a & 1;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          const int e = lane + 32 * i;
+          if (e < D) {
+            const float x0 = sg[XR + e], x1 = sg[XR + (e ^ 1)];
+            th[i] = fmaf(ca, ba ? ((e & 1) ? -x1 : x1) : x0, th[i]);
+          }
+        }
+        if (j == sa) {
+          Cout[a] = c;
+          FSout[a] = fs;
+          nact += fs >= 0;
+        }
+      }
+    }
+    sm = sm + 1 == R ? 0 : sm + 1;
+  }
+  cp_async_wait<0>();
+  // ---- samples still in the window after the last step ----
+  const int a0 = Np - W + 1 > 0 ? Np - W + 1 : 0;
+  if (samp >= a0 && samp < Np) {
+    Cout[samp] = c;
+    FSout[samp] = fs;
+    nact += fs >= 0;
+  }
+  atomicAdd(&red[0], nact);
+  atomicOr(&red[1], status);
+  __syncthreads();
+  if (warp == 0) {
+    const float* cl = csm + ((Np - 1) & 1) * R;
+    for (int a = a0; a < Np; ++a) {
+      const float ca = cl[a % R];
+      const float* xa = X + (long long)(a >> 1) * D;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int e = lane + 32 * i;
+        if (e < D) th[i] = fmaf(ca, rcomp(xa, e, a & 1), th[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int e = lane + 32 * i;
+      if (e < D)
+        theta_out[(long long)task * D + ((e & 1) ? M + (e >> 1) : (e >> 1))] = w_l * th[i];
+    }
+    if (lane == 0) {
+      nact_out[task] = red[0];
+      status_out[task] = red[1];
+    }
+  }
+}
+
 static int tp_num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -480,11 +869,15 @@ int screen_tc_rows(const float* rx, long long rx_stride, int F, int n_train, int
                    int y_row0, int list_max_off, int M, kapsm_kernel_params p, unsigned* live,
                    int* cnt, float4* vals, cudaStream_t s);
 
-// workspace carved out of the pipeline's Gram workspace: band rows, then the
-// pilot x pilot screen (live words, counts, lists)
-size_t train_tp_ws_bytes(int F, int n_train) {
-  const size_t Np = 2 * (size_t)n_train, NWp = (n_train + 31) / 32;
-  const size_t band = (F * Np * 32 * 4 + 255) / 256 * 256;
+// ring size of the chain's trainer: 32 (one warp) while P = 28 - W > TP_AHEAD,
+// else the wide trainer's 32 NW
+static int tp_ring(int W) { return tp_lead(W) > TP_AHEAD ? TP_RING : 32 * tpw_nw(W); }
+
+// workspace carved out of the pipeline's Gram workspace: band rows (R per
+// realified pilot), then the pilot x pilot screen (live words, counts, lists)
+size_t train_tp_ws_bytes(int F, int n_train, int W) {
+  const size_t Np = 2 * (size_t)n_train, NWp = (n_train + 31) / 32, R = tp_ring(W);
+  const size_t band = (F * Np * R * 4 + 255) / 256 * 256;
   const size_t live = (F * NWp * n_train * 4 + 255) / 256 * 256;
   const size_t cnt = (F * (size_t)n_train * 4 + 255) / 256 * 256;
   return band + live + cnt + F * (size_t)n_train * TP_CAP * 16;
@@ -492,9 +885,10 @@ size_t train_tp_ws_bytes(int F, int n_train) {
 
 bool train_tp_supported(int n_train, int M, int W) {
   // the live terms of a sample are added TP_AHEAD steps after its takeover, which
-  // must precede its entry into the window: P = TP_SPAN - W > TP_AHEAD
-  if (W < 1 || tp_lead(W) <= TP_AHEAD || M < 1 || M > 64 || n_train < 1) return false;
-  return tp_total(M) <= 200 * 1024;
+  // must precede its entry into the window: P = SPAN - W > TP_AHEAD
+  if (W < 1 || M < 1 || M > 64 || n_train < 1) return false;
+  if (tp_lead(W) > TP_AHEAD) return tp_total(M) <= 200 * 1024;
+  return tpw_nw(W) <= TPW_MAX_NW && tpw_total_rt(tpw_nw(W), M) <= 227 * 1024;
 }
 
 // stages (bit mask, all by default): 1 band rows, 2 pilot screen, 4 trainer --
@@ -504,10 +898,10 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
              void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
              cudaStream_t s, int stages = 7) {
   if (!train_tp_supported(n_train, M, W)) return KAPSM_ERR_UNSUPPORTED;
-  const int Np = 2 * n_train, NWp = (n_train + 31) / 32;
+  const int Np = 2 * n_train, NWp = (n_train + 31) / 32, R = tp_ring(W), SPAN = R - 4;
   char* w = reinterpret_cast<char*>(ws);
   float* kband = reinterpret_cast<float*>(w);
-  w += ((size_t)F * Np * 32 * 4 + 255) / 256 * 256;
+  w += ((size_t)F * Np * R * 4 + 255) / 256 * 256;
   unsigned* plive = reinterpret_cast<unsigned*>(w);
   w += ((size_t)F * NWp * n_train * 4 + 255) / 256 * 256;
   int* pcnt = reinterpret_cast<int*>(w);
@@ -515,42 +909,59 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
   float4* pvals = reinterpret_cast<float4*>(w);
   const float inv2s = (float)(1.0 / (2.0 * p.sigma_sq));
   if (stages & 1) {
-    dim3 grid((unsigned)((n_train * 17 + 255) / 256), F);
+    dim3 grid((unsigned)(((long long)n_train * (R / 2 + 1) + 255) / 256), F);
     band_kernel<<<grid, 256, 0, s>>>(rx, rx_stride, n_train, M, (float)p.w_l, (float)p.w_g, inv2s,
-                                     kband);
+                                     kband, R);
     if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
   }
   if ((stages & 2) && p.w_g != 0.0) {
-    // lists only hold pilots p <= t - TP_SPAN / 2 of row t: the trainer's live
-    // terms are the samples a <= m - TP_SPAN (the band rows cover the rest)
-    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, -(TP_SPAN / 2), M, p,
+    // lists only hold pilots p <= t - SPAN / 2 of row t: the trainer's live
+    // terms are the samples a <= m - SPAN (the band rows cover the rest)
+    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, -(SPAN / 2), M, p,
                                  plive, pcnt, pvals, s);
     if (r) return r;
   }
   if (!(stages & 4)) return KAPSM_OK;
   const int tasks = F * K;
+  const int DPL = (2 * M + 31) / 32;
   // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
   // so no other CTA (the concurrent detection screen) shares its SM;
   // throughput: 4 chains per CTA (several CTAs per SM)
   const bool lat = tasks <= tp_num_sms();
-  int wpc = lat ? 1 : 4;
-  while (wpc > 1 && (size_t)tp_total(M) * wpc > 227 * 1024) wpc >>= 1;
-  size_t smem = (size_t)tp_total(M) * wpc;
-  if (lat && smem < 120 * 1024) smem = 120 * 1024;
-  if (smem > 227 * 1024) return KAPSM_ERR_UNSUPPORTED;
-  const int DPL = (2 * M + 31) / 32;
-  auto launch = [&](auto kern) -> int {
+  auto launch = [&](auto kern, int wpc, int threads, size_t smem) -> int {
+    if (lat && smem < 120 * 1024) smem = 120 * 1024;
+    if (smem > 227 * 1024) return (int)KAPSM_ERR_UNSUPPORTED;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return (int)KAPSM_ERR_CUDA;
-    kern<<<(tasks + wpc - 1) / wpc, 32 * wpc, smem, s>>>(
+    kern<<<(tasks + wpc - 1) / wpc, threads, smem, s>>>(
         rx, rx_stride, targets, kband, plive, pcnt, pvals, F, K, n_train, M, W, (float)eps,
         (float)p.w_l, (float)p.w_g, inv2s, qtab, coeff, first_step, theta, n_active, status);
     return status_from(cudaGetLastError());
   };
-  if (DPL == 1) return launch(apsm_train_tp_kernel<1>);
-  if (DPL == 2) return launch(apsm_train_tp_kernel<2>);
-  return launch(apsm_train_tp_kernel<4>);
+  if (R == TP_RING) {
+    int wpc = lat ? 1 : 4;
+    while (wpc > 1 && (size_t)tp_total(M) * wpc > 227 * 1024) wpc >>= 1;
+    const size_t smem = (size_t)tp_total(M) * wpc;
+    if (DPL == 1) return launch(apsm_train_tp_kernel<1>, wpc, 32 * wpc, smem);
+    if (DPL == 2) return launch(apsm_train_tp_kernel<2>, wpc, 32 * wpc, smem);
+    return launch(apsm_train_tp_kernel<4>, wpc, 32 * wpc, smem);
+  }
+  // wide windows: one CTA of R / 32 warps per chain
+  const int NW = R / 32;
+  const size_t smem = (size_t)tpw_total_rt(NW, M);
+#define KAPSM_TPW(NWV)                                                                   \
+  if (NW == NWV) {                                                                       \
+    if (DPL == 1) return launch(apsm_train_tpw_kernel<1, NWV>, 1, 32 * NWV, smem);       \
+    if (DPL == 2) return launch(apsm_train_tpw_kernel<2, NWV>, 1, 32 * NWV, smem);       \
+    return launch(apsm_train_tpw_kernel<4, NWV>, 1, 32 * NWV, smem);                     \
+  }
+  KAPSM_TPW(2)
+  KAPSM_TPW(3)
+  KAPSM_TPW(4)
+  KAPSM_TPW(5)
+#undef KAPSM_TPW
+  return KAPSM_ERR_UNSUPPORTED;
 }
 
 }  // namespace kapsm
@@ -558,8 +969,8 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
 // Internal (bench stage timing, not in the public header): the throughput
 // trainer's stages alone -- band rows (1), pilot screen (2), trainer (4) -- on a
 // workspace of kapsm_internal_train_tp_ws_bytes bytes.
-extern "C" long long kapsm_internal_train_tp_ws_bytes(int F, int n_train) {
-  return (long long)kapsm::train_tp_ws_bytes(F, n_train);
+extern "C" long long kapsm_internal_train_tp_ws_bytes(int F, int n_train, int W) {
+  return (long long)kapsm::train_tp_ws_bytes(F, n_train, W);
 }
 extern "C" int kapsm_internal_train_tp_f32(int stages, const float* rx, long long rx_stride,
                                            const float* targets, int F, int K, int n_train, int M,

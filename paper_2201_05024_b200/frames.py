@@ -73,12 +73,10 @@ class FramePipeline:
         esz = 4 if precision == "f32" else 8
         ws = int(lib.kapsm_pipeline_workspace_bytes(F, K, n_train, M, self.cfg.window, esz))
         full = (F * self.Np + 32) * self.ld * esz
-        if full_workspace or ws >= full:
-            self._gram_buf = z(F * self.Np + 32, self.ld)
-            self.gram = self._gram_buf[: F * self.Np].view(F, self.Np, self.ld)
-        else:
-            self._gram_buf = z((ws + esz * self.ld - 1) // (esz * self.ld), self.ld)
-            self.gram = None
+        need = max(ws, full) if full_workspace else ws
+        self._gram_buf = z((need + esz * self.ld - 1) // (esz * self.ld), self.ld)
+        self.gram = (self._gram_buf[: F * self.Np].view(F, self.Np, self.ld)
+                     if self._gram_buf.shape[0] >= F * self.Np + 32 else None)
         self.coeff = z(F, K, self.Np)
         self.first_step = z(F, K, self.Np, dt=torch.int32)
         self.theta = z(F, K, 2 * M)
@@ -163,6 +161,10 @@ class FramePipeline:
             raise ValueError("launch_trainer needs the overlapped FP32 pipeline")
         if mode == 1 and self.gram is None:
             raise ValueError("the Gram-based trainer needs FramePipeline(full_workspace=True)")
+        lib = _lib.load()
+        if mode == 2 and int(lib.kapsm_internal_train_tp_ws_bytes(self.F, self.n_train, self.cfg.window)) > \
+                self._gram_buf.numel() * self._gram_buf.element_size():
+            raise ValueError("workspace too small for the one-warp trainer")
         _lib.check(_lib.load().kapsm_internal_run_frames_overlap_mode_f32(
             int(mode), *self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
             "run_frames_overlap_mode")

@@ -1,0 +1,35 @@
+"""Time one of bench.py's OTHER_CONFIGS single-frame pipelines with each
+trainer (AUTO / Gram / one-warp), CUDA events around one launch.
+usage: python tools/cfg_time.py NAME [reps]"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import bench
+import paper_2201_05024_b200 as K
+
+name = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+c = bench.OTHER_CONFIGS[name]
+rx, pil, tx, _ = K.host_frames([3], c["K"], c["M"], c["n_train"], c["n_data"], c["scheme"])
+p = K.FramePipeline(1, c["K"], c["M"], c["n_train"], c["n_data"], c["scheme"],
+                    cfg=K.ApsmConfig(window=c["W"]), precision="f32", store_est=False,
+                    full_workspace="gram" in sys.argv)
+p.load(rx, pil, tx)
+modes = [("auto", p.launch)] + ([("gram", lambda: p.launch_trainer(1))] if p.gram is not None else []) \
+    + [("tp", lambda: p.launch_trainer(2))]
+for label, fn in modes:
+    try:
+        fn()
+    except Exception as e:            # noqa: BLE001
+        print(label, "unavailable:", e)
+        continue
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    r = p.results()
+    print(name, label, "us", [round(t) for t in ts], "bit_err", int(r["bit_err"].sum()),
+          "atoms", r["n_active"][0].tolist()[:4], flush=True)
