@@ -33,7 +33,7 @@ static int pipe_num_sms() {
 // Gram workspace.  Latency mode keeps the Gram-based trainer, whose critical
 // warp is the shorter per-step chain when a chain has SMs to itself.
 // trainer choice: AUTO as above, or forced (internal entry points: tests, A/B)
-enum TrainerMode { TRAINER_AUTO = 0, TRAINER_GRAM = 1, TRAINER_TP = 2 };
+enum TrainerMode { TRAINER_AUTO = 0, TRAINER_GRAM = 1, TRAINER_TP = 2, TRAINER_TP1 = 3 };
 
 template <typename T>
 static bool use_tp(int F, int K, int n_train, int M, int window, long long ld,
@@ -43,7 +43,7 @@ static bool use_tp(int F, int K, int n_train, int M, int window, long long ld,
     return false;
   } else {
     if (mode == TRAINER_GRAM || !kapsm::train_tp_supported(n_train, M, window)) return false;
-    return mode == TRAINER_TP || (long long)F * K > pipe_num_sms() ||
+    return mode == TRAINER_TP || mode == TRAINER_TP1 || (long long)F * K > pipe_num_sms() ||
            kapsm::train_takes_general<float>(2 * n_train, window);
   }
 }
@@ -168,7 +168,8 @@ static int run_frames_overlap(const T* rx, long long rx_stride, const T* pilots,
         if ((r = Fns<T>::screen(rx, rx_stride, F, n_train, n_data, M, p, live_ws, s2))) break;
         if (cudaEventRecord(join, s2) != cudaSuccess) { r = KAPSM_ERR_CUDA; break; }
         if ((r = kapsm::train_tp(rx, rx_stride, pilots, F, K, n_train, M, window, eps, p, qtab,
-                                 gram_ws, coeff, first_step, theta, n_active, status, s)))
+                                 gram_ws, coeff, first_step, theta, n_active, status, s,
+                                 MODE == TRAINER_TP1 ? 15 : 7)))
           break;
         goto finish;
       }
@@ -227,7 +228,8 @@ KAPSM_RUN2_ENTRY(kapsm_run_frames_overlap_f64, double)
 // Internal (tests / A-B timing, not in the public header): the overlapped
 // pipeline in FP32 with the trainer forced -- mode 1: the Gram-based trainer
 // (K1 pilot Gram + K2 train.cu), mode 2: the one-warp-per-chain trainer
-// (train_tp.cu) whenever its limits hold, at any number of chains.
+// (train_tp.cu) whenever its limits hold, at any number of chains (its
+// critical-warp form in latency mode), mode 3: as 2 without that form.
 extern "C" int kapsm_internal_run_frames_overlap_mode_f32(
     int mode, const float* rx, long long rx_stride, const float* pilots,
     const unsigned char* tx_labels, int F, int K, int n_train, int n_data, int M, int window,
@@ -242,6 +244,7 @@ extern "C" int kapsm_internal_run_frames_overlap_mode_f32(
                                        labels, bit_err, sym_err, stream, side_stream)
   if (mode == TRAINER_GRAM) KAPSM_MODE_CALL(TRAINER_GRAM);
   if (mode == TRAINER_TP) KAPSM_MODE_CALL(TRAINER_TP);
+  if (mode == TRAINER_TP1) KAPSM_MODE_CALL(TRAINER_TP1);
 #undef KAPSM_MODE_CALL
   return KAPSM_ERR_INVALID;
 }

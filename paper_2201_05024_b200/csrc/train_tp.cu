@@ -30,6 +30,8 @@
 // row, target and live count), so the chain never waits on memory.
 #include "kapsm_common.cuh"
 
+#include <type_traits>
+
 namespace kapsm {
 
 constexpr int TP_RING = 32;
@@ -854,6 +856,369 @@ __global__ void __launch_bounds__(32 * NW, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2l: the band trainer for latency mode (a chain per SM): the same restated
+// recurrence as K2t, with the work that does not feed the next step moved off
+// the critical warp.
+//   * warp 0 (critical) owns the ring (lane = slot, 32 slots, W <= 21).  Per
+//     step: the delta of its slot, the window update of every slot's response
+//     (K over ring pairs in shared memory), the takeover of sample m = n + P
+//     (K's new row/column from the band row, and the products c_j K[j][m] of
+//     the window's current coefficients -> the p ring), the init of the sample
+//     entering at step n + 1 added to its response, the leaving sample's final
+//     coefficient -> cfin (shared) and the outputs;
+//   * warps 1..3 (helpers, sample m handled by helper m mod 3) prefetch every
+//     stage (pilot row, band row, live list, target) with cp.async 18 samples
+//     ahead and publish it by tag 6 samples ahead of their own work, keep a replica of theta_fin (final
+//     coefficients of the samples that left the window, times their rows), and
+//     form sample m's init
+//         w_l theta_fin . r_m + sum_j p[m][j] + w_g sum_live c_a kappa(r_a, r_m)
+//     once the critical warp has taken m over; published as a tagged value,
+//     added by the critical warp one step before m enters the window (P - 1
+//     steps of slack).
+// The critical warp's response of m starts at 0 at the takeover and gathers
+// the window updates from there, so the init only has to arrive before step m.
+// Shared-memory hand-offs are tagged values (one 64-bit store) or tags written
+// after a block fence; the critical warp only spins when a helper is late.
+constexpr int TPL_STG = 64;              // stages (samples) kept: prefetch lead + leaving rows
+constexpr int TPL_NH = 3;                // helper warps
+constexpr int TPL_J = 6;                 // prefetch depth per helper (TPL_NH x TPL_J samples);
+                                         // stages published 2 own samples ahead
+constexpr int TPL_MAXNP = 16384;         // final coefficients kept in shared memory
+
+template <int KPL>
+struct TplL {
+  static constexpr int XR = 64 * KPL;                       // pilot row (2M <= 64 KPL floats)
+  static constexpr int SSTR = XR + 68;                      // row, band 32, live list 32, B, LC
+  static constexpr int OKB = XR, OLV = XR + 32, OB = XR + 64, OLC = XR + 65;
+  static constexpr int KS = 0;                              // [32][TP_KS] K over ring pairs
+  static constexpr int DSM = KS + TP_RING * TP_KS * 4;      // [32] deltas
+  static constexpr int QS = DSM + 128;                      // [32][2] (q_mid, q_last)
+  static constexpr int INIT = QS + 256;                     // [32] tagged inits
+  static constexpr int PR = INIT + 256;                     // [64][32] tagged c_j K[j][m]
+  static constexpr int STAG = PR + 64 * 32 * 8;             // [TPL_STG] stage tags
+  static constexpr int RED = STAG + TPL_STG * 4;            // nact, status
+  static constexpr int STG = RED + 16;                      // [TPL_STG][SSTR] stages
+  static constexpr int CFIN = STG + TPL_STG * SSTR * 4;     // [Np] final coefficients
+  static size_t bytes(int Np) { return (size_t)CFIN + (size_t)Np * 4; }
+};
+__host__ __device__ constexpr int tpl_kpl(int M) { return (M + 31) / 32; }
+
+template <int KPL>
+__global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
+    apsm_train_tpl_kernel(const float* __restrict__ rx, long long rx_stride,
+                          const float* __restrict__ targets, const float* __restrict__ kband,
+                          const unsigned* __restrict__ plive, const int* __restrict__ pcnt,
+                          const float4* __restrict__ pvals, int F, int K, int n_train, int M,
+                          int W, float eps, float w_l, float w_g, float inv2s,
+                          const float* __restrict__ qtab, float* __restrict__ coeff_out,
+                          int* __restrict__ fs_out, float* __restrict__ theta_out,
+                          int* __restrict__ nact_out, int* __restrict__ status_out) {
+  extern __shared__ __align__(128) unsigned char smem_tp[];
+  using L = TplL<KPL>;
+  constexpr int XR = L::XR, SSTR = L::SSTR, OKB = L::OKB, OLV = L::OLV, OB = L::OB,
+                OLC = L::OLC;
+  const int Np = 2 * n_train, D = 2 * M, P = tp_lead(W);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x;
+  if (task >= F * K) return;
+  const unsigned sb = smem_u32(smem_tp);
+  float* Ks = reinterpret_cast<float*>(smem_tp + L::KS);
+  float* dsm = reinterpret_cast<float*>(smem_tp + L::DSM);
+  float* qs = reinterpret_cast<float*>(smem_tp + L::QS);
+  int* stag = reinterpret_cast<int*>(smem_tp + L::STAG);
+  int* red = reinterpret_cast<int*>(smem_tp + L::RED);
+  const float* Sg = reinterpret_cast<const float*>(smem_tp + L::STG);
+  float* cfin = reinterpret_cast<float*>(smem_tp + L::CFIN);
+  const unsigned s_init = sb + L::INIT, s_pr = sb + L::PR;
+  const int f = task / K;
+  const float* X = rx + (long long)f * rx_stride;
+  const float* Bt = targets + (long long)task * Np;
+  const float* KB = kband + (long long)f * Np * 32;
+  const int NWp = (n_train + 31) / 32;
+  const unsigned* LW = plive + (long long)f * NWp * n_train;
+  const int* LC = pcnt + (long long)f * n_train;
+  const float4* LV = pvals + (long long)f * n_train * TP_CAP;
+  float* Cout = coeff_out + (long long)task * Np;
+  int* FSout = fs_out + (long long)task * Np;
+  const bool gauss = w_g != 0.f;
+
+  for (int i = threadIdx.x; i < TP_RING * TP_KS; i += blockDim.x) Ks[i] = 0.f;
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+    dsm[i] = 0.f;
+    st_tag(s_init + 8u * i, 0.f, -1);
+  }
+  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) st_tag(s_pr + 8u * i, 0.f, -1);
+  for (int i = threadIdx.x; i < TPL_STG; i += blockDim.x) stag[i] = -1;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
+    qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
+  }
+  if (threadIdx.x == 0) red[0] = red[1] = 0;
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= critical warp =================
+    // steps as straight-line code (takeover / delta parts selected at compile
+    // time for the warm-up, main and tail ranges); the tags it depends on are
+    // loaded at the top of a step and tested at its end: the init of the sample
+    // entering next, and the stage TPL_LA samples ahead of the takeover
+    constexpr int TPL_LA = 2;
+    float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
+    int samp = -(1 << 30), fs = -1, nact = 0, status = 0;
+    const unsigned krow = sb + L::KS + (unsigned)(lane * TP_KS) * 4;
+    const unsigned dsa = sb + L::DSM;
+    for (int s = 0; s < TPL_LA && s < Np; ++s)
+      while (ld_volatile(stag + s) != s) {
+      }
+    auto step = [&](const int n, auto tk, auto dl_on, auto qconst) {
+      const int m = n + P, e = n + 1, a = n - W + 1;
+      float iv;
+      int itag;
+      ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
+      const int la = m + TPL_LA;
+      const int sgtag = ld_volatile(stag + (la & (TPL_STG - 1)));
+      if constexpr (decltype(tk)::value) {       // ---- takeover of sample m ----
+        const int sm = m & 31;
+        const float* sg = Sg + (m & (TPL_STG - 1)) * SSTR;
+        const float v = sg[OKB + ((sm - lane) & 31)];      // K[m][this lane's sample]
+        Ks[sm * TP_KS + lane] = v;
+        Ks[lane * TP_KS + sm] = v;
+        const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);
+        st_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), win ? c * v : 0.f, m);
+        const float b = sg[OB];
+        const bool mine = lane == sm;
+        samp = mine ? m : samp;
+        Y = mine ? 0.f : Y;
+        c = mine ? 0.f : c;
+        fs = mine ? -1 : fs;
+        status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;
+        const float rv = __fdividef(1.f, v);
+        idn = mine ? (v > 0.f ? rv : 0.f) : idn;
+        bl = mine ? b - eps : bl;
+        bh = mine ? b + eps : bh;
+      }
+      if constexpr (decltype(dl_on)::value) {    // ---- step n: my slot's delta ----
+        const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
+        float qm, ql;
+        if constexpr (decltype(qconst)::value) {
+          qm = qs[2 * (W - 1)];
+          ql = qs[2 * (W - 1) + 1];
+        } else {
+          qm = qs[2 * cj];
+          ql = qs[2 * cj + 1];
+        }
+        const float q = samp == n ? ql : qm;
+        const bool inw = (unsigned)(samp - lo) <= (unsigned)cj;
+        float dl = q * idn * (fmaxf(bl - Y, 0.f) + fminf(bh - Y, 0.f));
+        dl = inw ? dl : 0.f;
+        c += dl;
+        fs = (dl != 0.f && fs < 0) ? n : fs;
+        dsm[lane] = dl;
+      }
+      __syncwarp();                              // deltas and the takeover's K row/column
+      if constexpr (decltype(dl_on)::value) {
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+        for (int s = 0; s < 32; s += 8) {
+          const float4 d0 = lds_f4(dsa + 4u * s), k0 = lds_f4(krow + 4u * s);
+          const float4 d1 = lds_f4(dsa + 4u * (s + 4)), k1 = lds_f4(krow + 4u * (s + 4));
+          a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+          a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+          a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+          a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+        }
+        Y += ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+      }
+      if (e >= 0 && e < Np) {                    // the sample entering at step e: its init
+        while (itag != e) ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
+        Y += lane == (e & 31) ? iv : 0.f;
+      }
+      const bool own = a >= 0 && lane == (a & 31);   // leaves after this step: c is final
+      if (own) cfin[a] = c;
+      stg_if(own, Cout + a, c);
+      stg_if(own, FSout + a, fs);
+      nact += (own && fs >= 0) ? 1 : 0;
+      if (la < Np)
+        while (sgtag != la && ld_volatile(stag + (la & (TPL_STG - 1))) != la) {
+        }
+      __syncwarp();                              // delta reads done before the next writes
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    int n = -P;
+    for (; n < 0 && n + P < Np; ++n) step(n, T_{}, F_{}, F_{});             // warm-up: takeovers
+    for (; n < W - 1 && n + P < Np; ++n) step(n, T_{}, T_{}, F_{});         // window filling
+    for (; n + P < Np; ++n) step(n, T_{}, T_{}, T_{});                      // main
+    for (; n < 0; ++n) step(n, F_{}, F_{}, F_{});                           // (Np <= P)
+    for (; n < Np; ++n) step(n, F_{}, T_{}, F_{});                          // tail: no takeover
+    if (samp >= 0 && samp < Np && samp > Np - W) {   // still in the window after the last step
+      cfin[samp] = c;
+      Cout[samp] = c;
+      FSout[samp] = fs;
+      nact += fs >= 0;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      nact += __shfl_xor_sync(0xffffffffu, nact, o);
+      status |= __shfl_xor_sync(0xffffffffu, status, o);
+    }
+    if (lane == 0) {
+      red[0] = nact;
+      red[1] = status;
+    }
+    named_bar(1, 32 * (1 + TPL_NH));
+  } else {
+    // ================= helper warps =================
+    const int h = warp - 1;
+    const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
+    const int XP = vec ? D / 4 : D, NPC = XP + 18;
+    const unsigned sg_s = sb + L::STG;
+    // stage of sample s: pilot row, band row, live list, target, live count
+    auto prefetch = [&](int s) {
+      if (s < Np) {
+        const unsigned so = sg_s + (unsigned)((s & (TPL_STG - 1)) * SSTR) * 4;
+        const int t = s >> 1;
+        for (int pc = lane; pc < NPC; pc += 32) {
+          if (pc < XP) {
+            if (vec) cpa16(so + 16u * pc, X + (long long)t * D + 4 * pc);
+            else cpa4(so + 4u * pc, X + (long long)t * D + pc);
+          } else if (pc < XP + 8) {
+            const int q = pc - XP;
+            cpa16(so + (unsigned)(OKB + 4 * q) * 4, KB + (long long)s * 32 + 4 * q);
+          } else if (pc < XP + 16) {
+            const int q = pc - XP - 8;
+            if (gauss) cpa16(so + (unsigned)(OLV + 4 * q) * 4, LV + (long long)t * TP_CAP + q);
+          } else if (pc == XP + 16) {
+            cpa4(so + (unsigned)OB * 4, Bt + s);
+          } else if (gauss) {
+            cpa4(so + (unsigned)OLC * 4, LC + t);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    for (int j = 0; j < TPL_J; ++j) prefetch(h + TPL_NH * j);
+    cp_async_wait<TPL_J - 2>();                 // my stages of h and h + NH landed
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0 && h < Np) st_volatile(stag + (h & (TPL_STG - 1)), h);
+    if (lane == 0 && h + TPL_NH < Np)
+      st_volatile(stag + ((h + TPL_NH) & (TPL_STG - 1)), h + TPL_NH);
+    float2 th[KPL];                              // (Re, Im) of antenna lane + 32 i
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) th[i] = make_float2(0.f, 0.f);
+    int next_a = 0;
+    for (int m = h; m < Np; m += TPL_NH) {
+      prefetch(m + TPL_NH * TPL_J);
+      cp_async_wait<TPL_J - 2>();               // my stage of sample m + 2 NH landed
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0 && m + 2 * TPL_NH < Np)
+        st_volatile(stag + ((m + 2 * TPL_NH) & (TPL_STG - 1)), m + 2 * TPL_NH);
+      float pv;                                 // c_j K[j][m]: written at m's takeover
+      while (!ld_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), m, pv)) {
+      }
+      __syncwarp();
+      // theta_fin: the samples a <= m - SPAN (left the window by m's takeover)
+      for (; next_a <= m - TP_SPAN; ++next_a) {
+        const int a = next_a;
+        const float ca = cfin[a];
+        const float* xa = Sg + (a & (TPL_STG - 1)) * SSTR;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          const int k = lane + 32 * i;
+          if (k < M) {
+            const float xr = xa[2 * k], xi = xa[2 * k + 1];
+            // r1 = [Re; Im], r2 = [Im; -Re] (apsm.py:156-169)
+            th[i].x = fmaf(ca, (a & 1) ? xi : xr, th[i].x);
+            th[i].y = fmaf(ca, (a & 1) ? -xr : xi, th[i].y);
+          }
+        }
+      }
+      const float* sm_ = Sg + (m & (TPL_STG - 1)) * SSTR;
+      float part = pv, lin = 0.f;
+      const int bt = m & 1;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        const int k = lane + 32 * i;
+        if (k < M) {
+          const float xr = sm_[2 * k], xi = sm_[2 * k + 1];
+          lin = fmaf(th[i].x, bt ? xi : xr, lin);
+          lin = fmaf(th[i].y, bt ? -xr : xi, lin);
+        }
+      }
+      part = fmaf(w_l, lin, part);
+      if (gauss) {                              // live Gaussian terms of older samples
+        const int cnt = __float_as_int(sm_[OLC]);
+        if (cnt > 0) {
+          if (lane < 2 * cnt) {
+            const float4 v4 = reinterpret_cast<const float4*>(sm_ + OLV)[lane >> 1];
+            const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
+            if (a <= m - TP_SPAN) {
+              const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
+              part = fmaf(w_g * cfin[a], kap, part);
+            }
+          }
+        } else if (cnt < 0) {                   // more live pilots than the list holds
+          const int tl = m >> 1;
+          const float* xm = X + (long long)tl * D;
+          for (int w = lane; w < NWp; w += 32) {
+            unsigned bits = LW[(long long)w * n_train + tl];
+            while (bits) {
+              const int p = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const float* xa = X + (long long)p * D;
+              for (int al = 0; al < 2; ++al) {
+                const int a = 2 * p + al;
+                if (a > m - TP_SPAN) continue;
+                float dist = 0.f;
+                for (int e2 = 0; e2 < D; ++e2) {
+                  const float z = rcomp(xa, e2, al) - rcomp(xm, e2, bt);
+                  dist = fmaf(z, z, dist);
+                }
+                part = fmaf(w_g * cfin[a], exp_fast(-dist * inv2s), part);
+              }
+            }
+          }
+        }
+      }
+      const float init = warp_sum_f(part);
+      if (lane == 0) st_tag(s_init + 8u * (unsigned)(m & 31), init, m);
+    }
+    cp_async_wait<0>();
+    named_bar(1, 32 * (1 + TPL_NH));
+    if (h == 0) {                               // theta = w_l (all final c_a r_a)
+      for (; next_a < Np; ++next_a) {
+        const int a = next_a;
+        const float ca = cfin[a];
+        const float* xa = X + (long long)(a >> 1) * D;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          const int k = lane + 32 * i;
+          if (k < M) {
+            const float xr = xa[2 * k], xi = xa[2 * k + 1];
+            th[i].x = fmaf(ca, (a & 1) ? xi : xr, th[i].x);
+            th[i].y = fmaf(ca, (a & 1) ? -xr : xi, th[i].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        const int k = lane + 32 * i;
+        if (k < M) {
+          theta_out[(long long)task * D + k] = w_l * th[i].x;
+          theta_out[(long long)task * D + M + k] = w_l * th[i].y;
+        }
+      }
+      if (lane == 0) {
+        nact_out[task] = red[0];
+        status_out[task] = red[1];
+      }
+    }
+  }
+}
+
 static int tp_num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -892,7 +1257,8 @@ bool train_tp_supported(int n_train, int M, int W) {
 }
 
 // stages (bit mask, all by default): 1 band rows, 2 pilot screen, 4 trainer --
-// separate launches so the bench can time each on its stream
+// separate launches so the bench can time each on its stream; 8: no
+// critical-warp form in latency mode (A/B)
 int train_tp(const float* rx, long long rx_stride, const float* targets, int F, int K,
              int n_train, int M, int W, double eps, kapsm_kernel_params p, const float* qtab,
              void* ws, float* coeff, int* first_step, float* theta, int* n_active, int* status,
@@ -939,6 +1305,17 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
         (float)p.w_l, (float)p.w_g, inv2s, qtab, coeff, first_step, theta, n_active, status);
     return status_from(cudaGetLastError());
   };
+  // latency mode: the critical-warp + helpers form (stages bit 8: the plain
+  // one-warp form instead, for A/B tests)
+  const int Np2 = 2 * n_train;
+  if (R == TP_RING && lat && !(stages & 8) && Np2 <= TPL_MAXNP) {
+    const int KPL = tpl_kpl(M);
+    const size_t smem = KPL == 1 ? TplL<1>::bytes(Np2) : TplL<2>::bytes(Np2);
+    if (smem <= 227 * 1024) {
+      if (KPL == 1) return launch(apsm_train_tpl_kernel<1>, 1, 32 * (1 + TPL_NH), smem);
+      return launch(apsm_train_tpl_kernel<2>, 1, 32 * (1 + TPL_NH), smem);
+    }
+  }
   if (R == TP_RING) {
     int wpc = lat ? 1 : 4;
     while (wpc > 1 && (size_t)tp_total(M) * wpc > 227 * 1024) wpc >>= 1;

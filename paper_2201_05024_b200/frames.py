@@ -155,14 +155,15 @@ class FramePipeline:
 
     def launch_trainer(self, mode: int):
         """Internal (tests, A/B timing): the overlapped FP32 pipeline with the
-        trainer forced -- 1: Gram-based (train.cu), 2: one warp per chain
-        (train_tp.cu) at any number of chains."""
+        trainer forced -- 1: Gram-based (train.cu), 2: band trainer
+        (train_tp.cu) at any number of chains (its critical-warp + helpers form
+        in latency mode), 3: as 2 with the plain one-warp form."""
         if self.prec != "f32" or not self.overlap:
             raise ValueError("launch_trainer needs the overlapped FP32 pipeline")
         if mode == 1 and self.gram is None:
             raise ValueError("the Gram-based trainer needs FramePipeline(full_workspace=True)")
         lib = _lib.load()
-        if mode == 2 and int(lib.kapsm_internal_train_tp_ws_bytes(self.F, self.n_train, self.cfg.window)) > \
+        if mode in (2, 3) and int(lib.kapsm_internal_train_tp_ws_bytes(self.F, self.n_train, self.cfg.window)) > \
                 self._gram_buf.numel() * self._gram_buf.element_size():
             raise ValueError("workspace too small for the one-warp trainer")
         _lib.check(_lib.load().kapsm_internal_run_frames_overlap_mode_f32(

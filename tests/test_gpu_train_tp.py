@@ -27,16 +27,19 @@ def _oracle_users(rx, sym, nt, W, users):
     return [O.train_user(R, O.realify_targets(sym[u, :nt]), W=W) for u in users]
 
 
-@pytest.mark.parametrize("W", [20, 7, 21, 25, 53, 54, 120])
+@pytest.mark.parametrize("W,mode", [(20, 2), (7, 2), (21, 2), (20, 3), (7, 3), (25, 2), (53, 2),
+                                    (54, 2), (120, 2)])
 @pytest.mark.parametrize("path", SMALL, ids=[os.path.basename(p) for p in SMALL])
-def test_tp_trainer_matches_oracle(path, W):
+def test_tp_trainer_matches_oracle(path, W, mode):
+    """Single frames (latency mode): mode 2 = the critical-warp + helpers form
+    for W <= 21 and the wide ring beyond, mode 3 = the plain one-warp form."""
     g = np.load(path)
     Kn, M, nt, nd, sch = int(g["K"]), int(g["M"]), int(g["n_train"]), int(g["n_data"]), str(g["scheme"])
     fr = O.make_frame(int(g["seed"]), Kn, M, nt, nd, sch)
     rx, pil, tx, _ = K.host_frames([int(g["seed"])], Kn, M, nt, nd, sch)
     pipe = K.FramePipeline(1, Kn, M, nt, nd, sch, cfg=K.ApsmConfig(window=W), precision="f32")
     pipe.load(rx, pil, tx)
-    pipe.launch_trainer(2)                 # the one-warp-per-chain trainer
+    pipe.launch_trainer(mode)
     r = pipe.results()
     for u, ref in enumerate(_oracle_users(fr["rx"], fr["symbols"], nt, W, range(Kn))):
         assert int(r["n_active"][0, u]) == ref["n_atoms"], (u, W)
