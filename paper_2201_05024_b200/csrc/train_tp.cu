@@ -880,9 +880,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
 // the window updates from there, so the init only has to arrive before step m.
 // Shared-memory hand-offs are tagged values (one 64-bit store) or tags written
 // after a block fence; the critical warp only spins when a helper is late.
-constexpr int TPL_STG = 64;              // stages (samples) kept: prefetch lead + leaving rows
-constexpr int TPL_NH = 3;                // helper warps
-constexpr int TPL_J = 6;                 // prefetch depth per helper (TPL_NH x TPL_J samples);
+constexpr int TPL_STG = 128;             // stages (samples) kept: prefetch lead + leaving rows
+constexpr int TPL_NH = 7;                // helper warps
+constexpr int TPL_J = 3;                 // prefetch depth per helper (TPL_NH x TPL_J samples);
                                          // stages published 2 own samples ahead
 constexpr int TPL_MAXNP = 16384;         // final coefficients kept in shared memory
 
@@ -898,7 +898,8 @@ struct TplL {
   static constexpr int PR = INIT + 256;                     // [64][32] tagged c_j K[j][m]
   static constexpr int STAG = PR + 64 * 32 * 8;             // [TPL_STG] stage tags
   static constexpr int RED = STAG + TPL_STG * 4;            // nact, status
-  static constexpr int STG = RED + 16;                      // [TPL_STG][SSTR] stages
+  static constexpr int TKB = RED + 16;                      // [64] mbarriers: m taken over
+  static constexpr int STG = TKB + 64 * 8;                  // [TPL_STG][SSTR] stages
   static constexpr int CFIN = STG + TPL_STG * SSTR * 4;     // [Np] final coefficients
   static size_t bytes(int Np) { return (size_t)CFIN + (size_t)Np * 4; }
 };
@@ -954,8 +955,14 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
     qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
     qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
   }
-  if (threadIdx.x == 0) red[0] = red[1] = 0;
+  if (threadIdx.x == 0) {
+    red[0] = red[1] = 0;
+    for (int i = 0; i < 64; ++i)
+      mbar_init(reinterpret_cast<unsigned long long*>(smem_tp + L::TKB) + i, 1);
+    mbar_fence_init();
+  }
   __syncthreads();
+  const unsigned s_tkb = sb + L::TKB;
 
   if (warp == 0) {
     // ================= critical warp =================
@@ -968,42 +975,20 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
     int samp = -(1 << 30), fs = -1, nact = 0, status = 0;
     const unsigned krow = sb + L::KS + (unsigned)(lane * TP_KS) * 4;
     const unsigned dsa = sb + L::DSM;
+    const float qmc = qs[2 * (W - 1)], qlc = qs[2 * (W - 1) + 1];
     for (int s = 0; s < TPL_LA && s < Np; ++s)
       while (ld_volatile(stag + s) != s) {
       }
     auto step = [&](const int n, auto tk, auto dl_on, auto qconst) {
       const int m = n + P, e = n + 1, a = n - W + 1;
-      float iv;
-      int itag;
-      ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
-      const int la = m + TPL_LA;
-      const int sgtag = ld_volatile(stag + (la & (TPL_STG - 1)));
-      if constexpr (decltype(tk)::value) {       // ---- takeover of sample m ----
-        const int sm = m & 31;
-        const float* sg = Sg + (m & (TPL_STG - 1)) * SSTR;
-        const float v = sg[OKB + ((sm - lane) & 31)];      // K[m][this lane's sample]
-        Ks[sm * TP_KS + lane] = v;
-        Ks[lane * TP_KS + sm] = v;
-        const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);
-        st_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), win ? c * v : 0.f, m);
-        const float b = sg[OB];
-        const bool mine = lane == sm;
-        samp = mine ? m : samp;
-        Y = mine ? 0.f : Y;
-        c = mine ? 0.f : c;
-        fs = mine ? -1 : fs;
-        status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;
-        const float rv = __fdividef(1.f, v);
-        idn = mine ? (v > 0.f ? rv : 0.f) : idn;
-        bl = mine ? b - eps : bl;
-        bh = mine ? b + eps : bh;
-      }
-      if constexpr (decltype(dl_on)::value) {    // ---- step n: my slot's delta ----
+      // ---- step n: my slot's delta (the critical chain starts here) ----
+      float c_prev = c;
+      if constexpr (decltype(dl_on)::value) {
         const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
         float qm, ql;
         if constexpr (decltype(qconst)::value) {
-          qm = qs[2 * (W - 1)];
-          ql = qs[2 * (W - 1) + 1];
+          qm = qmc;
+          ql = qlc;
         } else {
           qm = qs[2 * cj];
           ql = qs[2 * cj + 1];
@@ -1016,7 +1001,47 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
         fs = (dl != 0.f && fs < 0) ? n : fs;
         dsm[lane] = dl;
       }
+      // tags this step depends on: the init of the sample entering at step e,
+      // and the stage TPL_LA samples ahead of the takeover
+      float iv;
+      int itag;
+      ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
+      const int la = m + TPL_LA;
+      const int sgtag = ld_volatile(stag + (la & (TPL_STG - 1)));
+      bool mine = false;
+      if constexpr (decltype(tk)::value) {       // ---- takeover of sample m ----
+        const int sm = m & 31;
+        const float* sg = Sg + (m & (TPL_STG - 1)) * SSTR;
+        const float v = sg[OKB + ((sm - lane) & 31)];      // K[m][this lane's sample]
+        Ks[sm * TP_KS + lane] = v;
+        Ks[lane * TP_KS + sm] = v;
+        // c_j K[j][m] of the window [n-W+1, n-1] before step n's deltas
+        const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);
+        st_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), win ? c_prev * v : 0.f, m);
+        const float b = sg[OB];
+        mine = lane == sm;
+        samp = mine ? m : samp;
+        c = mine ? 0.f : c;
+        fs = mine ? -1 : fs;
+        status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;
+        float rv;                                // MUFU on every lane: no branch
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"(v));
+        idn = mine ? (v > 0.f ? rv : 0.f) : idn;
+        bl = mine ? b - eps : bl;
+        bh = mine ? b + eps : bh;
+      }
       __syncwarp();                              // deltas and the takeover's K row/column
+      if constexpr (decltype(tk)::value) {       // m taken over: wake its helper
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];"
+                       ::"r"(s_tkb + 8u * (unsigned)(m & 63)) : "memory");
+      }
+      if (e >= 0 && e < Np && __any_sync(0xffffffffu, itag != e)) {
+        do {                                     // (a helper is late: rare)
+          ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
+        } while (__any_sync(0xffffffffu, itag != e));
+      }
+      const float add = (e >= 0 && e < Np && lane == (e & 31)) ? iv : 0.f;
       if constexpr (decltype(dl_on)::value) {
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
@@ -1028,20 +1053,20 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
           a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
           a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
         }
-        Y += ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
-      }
-      if (e >= 0 && e < Np) {                    // the sample entering at step e: its init
-        while (itag != e) ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
-        Y += lane == (e & 31) ? iv : 0.f;
+        const float upd = ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+        Y = (mine ? 0.f : Y) + (upd + add);      // the taken-over slot restarts at 0
+      } else {
+        Y = (mine ? 0.f : Y) + add;
       }
       const bool own = a >= 0 && lane == (a & 31);   // leaves after this step: c is final
       if (own) cfin[a] = c;
       stg_if(own, Cout + a, c);
       stg_if(own, FSout + a, fs);
       nact += (own && fs >= 0) ? 1 : 0;
-      if (la < Np)
-        while (sgtag != la && ld_volatile(stag + (la & (TPL_STG - 1))) != la) {
+      if (la < Np && __any_sync(0xffffffffu, sgtag != la)) {
+        while (ld_volatile(stag + (la & (TPL_STG - 1))) != la) {
         }
+      }
       __syncwarp();                              // delta reads done before the next writes
     };
     using T_ = std::true_type;
@@ -1074,26 +1099,57 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
     const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
     const int XP = vec ? D / 4 : D, NPC = XP + 18;
     const unsigned sg_s = sb + L::STG;
-    // stage of sample s: pilot row, band row, live list, target, live count
+    // stage of sample s: pilot row, band row, live list, target, live count;
+    // lane piece r (<= 5 per lane): shared offset, size, global address
+    // g + s * gs + (s >> 1) * gt
+    constexpr int PR_MAX = (2 * 64 * KPL + 18 + 31) / 32;
+    const char* pg[PR_MAX];
+    int pgs[PR_MAX], pgt[PR_MAX];
+    unsigned pso[PR_MAX];
+    int psz[PR_MAX];
+#pragma unroll
+    for (int r = 0; r < PR_MAX; ++r) {
+      const int pc = lane + 32 * r;
+      pg[r] = nullptr; pgs[r] = 0; pgt[r] = 0; pso[r] = 0; psz[r] = 0;
+      if (pc < XP) {
+        pg[r] = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
+        pgt[r] = D * 4;
+        pso[r] = (unsigned)(vec ? 16 * pc : 4 * pc);
+        psz[r] = vec ? 16 : 4;
+      } else if (pc < XP + 8) {
+        const int q = pc - XP;
+        pg[r] = reinterpret_cast<const char*>(KB + 4 * q);
+        pgs[r] = 128;
+        pso[r] = (unsigned)(OKB + 4 * q) * 4;
+        psz[r] = 16;
+      } else if (pc < XP + 16) {
+        const int q = pc - XP - 8;
+        pg[r] = reinterpret_cast<const char*>(LV + q);
+        pgt[r] = TP_CAP * 16;
+        pso[r] = (unsigned)(OLV + 4 * q) * 4;
+        psz[r] = gauss ? 16 : 0;
+      } else if (pc == XP + 16) {
+        pg[r] = reinterpret_cast<const char*>(Bt);
+        pgs[r] = 4;
+        pso[r] = (unsigned)OB * 4;
+        psz[r] = 4;
+      } else if (pc == XP + 17) {
+        pg[r] = reinterpret_cast<const char*>(LC);
+        pgt[r] = 4;
+        pso[r] = (unsigned)OLC * 4;
+        psz[r] = gauss ? 4 : 0;
+      }
+    }
+    const int nr = (NPC + 31) / 32;
     auto prefetch = [&](int s) {
-      if (s < Np) {
-        const unsigned so = sg_s + (unsigned)((s & (TPL_STG - 1)) * SSTR) * 4;
-        const int t = s >> 1;
-        for (int pc = lane; pc < NPC; pc += 32) {
-          if (pc < XP) {
-            if (vec) cpa16(so + 16u * pc, X + (long long)t * D + 4 * pc);
-            else cpa4(so + 4u * pc, X + (long long)t * D + pc);
-          } else if (pc < XP + 8) {
-            const int q = pc - XP;
-            cpa16(so + (unsigned)(OKB + 4 * q) * 4, KB + (long long)s * 32 + 4 * q);
-          } else if (pc < XP + 16) {
-            const int q = pc - XP - 8;
-            if (gauss) cpa16(so + (unsigned)(OLV + 4 * q) * 4, LV + (long long)t * TP_CAP + q);
-          } else if (pc == XP + 16) {
-            cpa4(so + (unsigned)OB * 4, Bt + s);
-          } else if (gauss) {
-            cpa4(so + (unsigned)OLC * 4, LC + t);
-          }
+      const unsigned so = sg_s + (unsigned)((s & (TPL_STG - 1)) * SSTR) * 4;
+      const bool in = s < Np;
+#pragma unroll
+      for (int r = 0; r < PR_MAX; ++r) {
+        if (r < nr) {
+          const char* g = pg[r] + (long long)s * pgs[r] + (long long)(s >> 1) * pgt[r];
+          cpa16_if(in && psz[r] == 16, so + pso[r], g);
+          cpa4_if(in && psz[r] == 4, so + pso[r], g);
         }
       }
       cp_async_commit();
@@ -1116,25 +1172,35 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
       __threadfence_block();
       if (lane == 0 && m + 2 * TPL_NH < Np)
         st_volatile(stag + ((m + 2 * TPL_NH) & (TPL_STG - 1)), m + 2 * TPL_NH);
-      float pv;                                 // c_j K[j][m]: written at m's takeover
+      // wait (suspended, not polling: no issue slots or shared-memory traffic
+      // taken from the critical warp) for m's takeover, then c_j K[j][m]
+      while (!mbar_try_wait_s(s_tkb + 8u * (unsigned)(m & 63), (unsigned)((m >> 6) & 1))) {
+      }
+      float pv;
       while (!ld_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), m, pv)) {
       }
       __syncwarp();
       // theta_fin: the samples a <= m - SPAN (left the window by m's takeover)
+      // (pairs of samples: 2t and 2t + 1 share the pilot row of t; a sample a
+      // adds c_a r1(x) (a even) or c_a r2(x) (a odd), r1 = [Re; Im],
+      // r2 = [Im; -Re], apsm.py:156-169)
       for (; next_a <= m - TP_SPAN; ++next_a) {
         const int a = next_a;
         const float ca = cfin[a];
+        const bool pair = (a & 1) == 0 && a + 1 <= m - TP_SPAN;
+        const float cb = pair ? cfin[a + 1] : 0.f;
+        const float ce = (a & 1) ? 0.f : ca, co = (a & 1) ? ca : cb;
         const float* xa = Sg + (a & (TPL_STG - 1)) * SSTR;
 #pragma unroll
         for (int i = 0; i < KPL; ++i) {
           const int k = lane + 32 * i;
           if (k < M) {
-            const float xr = xa[2 * k], xi = xa[2 * k + 1];
-            // r1 = [Re; Im], r2 = [Im; -Re] (apsm.py:156-169)
-            th[i].x = fmaf(ca, (a & 1) ? xi : xr, th[i].x);
-            th[i].y = fmaf(ca, (a & 1) ? -xr : xi, th[i].y);
+            const float2 x = *reinterpret_cast<const float2*>(xa + 2 * k);
+            th[i].x = fmaf(ce, x.x, fmaf(co, x.y, th[i].x));
+            th[i].y = fmaf(ce, x.y, fmaf(-co, x.x, th[i].y));
           }
         }
+        next_a += pair ? 1 : 0;
       }
       const float* sm_ = Sg + (m & (TPL_STG - 1)) * SSTR;
       float part = pv, lin = 0.f;
