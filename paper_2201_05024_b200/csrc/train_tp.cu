@@ -858,55 +858,62 @@ __global__ void __launch_bounds__(32 * NW, 1)
 
 // ---------------------------------------------------------------------------
 // K2l: the band trainer for latency mode (a chain per SM): the same restated
-// recurrence as K2t, with the work that does not feed the next step moved off
-// the critical warp.
-//   * warp 0 (critical) owns the ring (lane = slot, 32 slots, W <= 21).  Per
-//     step: the delta of its slot, the window update of every slot's response
-//     (K over ring pairs in shared memory), the takeover of sample m = n + P
-//     (K's new row/column from the band row, and the products c_j K[j][m] of
-//     the window's current coefficients -> the p ring), the init of the sample
-//     entering at step n + 1 added to its response, the leaving sample's final
-//     coefficient -> cfin (shared) and the outputs;
-//   * warps 1..3 (helpers, sample m handled by helper m mod 3) prefetch every
-//     stage (pilot row, band row, live list, target) with cp.async 18 samples
-//     ahead and publish it by tag 6 samples ahead of their own work, keep a replica of theta_fin (final
-//     coefficients of the samples that left the window, times their rows), and
-//     form sample m's init
+// recurrence as K2t / K2w, with the work that does not feed the next step
+// moved off the ring warps.
+//   * ring warps (NW of them; thread j owns ring slot j of R = 32 NW; takeover
+//     lead P = 28 - W for NW = 1, else 7).  Per step: the delta of its slot, one barrier among the ring
+//     warps (a __syncwarp for NW = 1), the window update of every slot's
+//     response (K over ring pairs in shared memory), the takeover of sample
+//     m = n + P (K's new row/column from the band row, and c_j K[j][m] of the
+//     window's current coefficients -> the p ring), the init of the sample
+//     entering at step n + 1 added to its response, and the leaving sample's
+//     final coefficient -> the cfin ring (shared) and the outputs;
+//   * TPL_NH helper warps (sample m handled by helper m mod TPL_NH) prefetch
+//     every stage (pilot row of m and of the sample leaving at m's takeover,
+//     band row, live list, target) with cp.async 21 samples ahead, publish it
+//     by tag 14 samples ahead of their own work, keep a replica of theta_fin
+//     (final coefficients of the samples that left the window, times their
+//     rows), and form sample m's init
 //         w_l theta_fin . r_m + sum_j p[m][j] + w_g sum_live c_a kappa(r_a, r_m)
-//     once the critical warp has taken m over; published as a tagged value,
-//     added by the critical warp one step before m enters the window (P - 1
-//     steps of slack).
-// The critical warp's response of m starts at 0 at the takeover and gathers
-// the window updates from there, so the init only has to arrive before step m.
-// Shared-memory hand-offs are tagged values (one 64-bit store) or tags written
-// after a block fence; the critical warp only spins when a helper is late.
-constexpr int TPL_STG = 128;             // stages (samples) kept: prefetch lead + leaving rows
+//     once m is taken over (an mbarrier the ring warps arrive on: the helpers
+//     sleep in hardware instead of polling shared memory), published as a
+//     tagged value, added by the ring warps one step before m enters the
+//     window (P - 1 steps of slack).
+// A slot's response restarts at 0 at the takeover and gathers the window
+// updates from there, so the init only has to arrive before step m.
+constexpr int TPL_STG = 64;              // stages (samples) in flight
 constexpr int TPL_NH = 7;                // helper warps
 constexpr int TPL_J = 3;                 // prefetch depth per helper (TPL_NH x TPL_J samples);
                                          // stages published 2 own samples ahead
-constexpr int TPL_MAXNP = 16384;         // final coefficients kept in shared memory
+constexpr int TPL_CFR = 256;             // ring of final coefficients (theta catch-up)
 
-template <int KPL>
+template <int KPL, int NW>
 struct TplL {
+  static constexpr int R = 32 * NW, KS = NW == 1 ? TP_KS : R + 4;
   static constexpr int XR = 64 * KPL;                       // pilot row (2M <= 64 KPL floats)
-  static constexpr int SSTR = XR + 68;                      // row, band 32, live list 32, B, LC
-  static constexpr int OKB = XR, OLV = XR + 32, OB = XR + 64, OLC = XR + 65;
-  static constexpr int KS = 0;                              // [32][TP_KS] K over ring pairs
-  static constexpr int DSM = KS + TP_RING * TP_KS * 4;      // [32] deltas
-  static constexpr int QS = DSM + 128;                      // [32][2] (q_mid, q_last)
-  static constexpr int INIT = QS + 256;                     // [32] tagged inits
-  static constexpr int PR = INIT + 256;                     // [64][32] tagged c_j K[j][m]
-  static constexpr int STAG = PR + 64 * 32 * 8;             // [TPL_STG] stage tags
+  static constexpr int SSTR = 2 * XR + R + 36;              // 2 rows, band R, live list 32, B, LC
+  static constexpr int OLR = XR, OKB = 2 * XR, OLV = OKB + R, OB = OLV + 32, OLC = OB + 1;
+  static constexpr int KSO = 0;                             // [R][KS] K over ring pairs
+  static constexpr int DSM = KSO + R * KS * 4;              // [2][R] deltas (by step parity)
+  static constexpr int QS = DSM + 2 * R * 4;                // [R][2] (q_mid, q_last)
+  static constexpr int INIT = QS + 2 * R * 4;               // [32] tagged inits
+  static constexpr int PR = INIT + 32 * 8;                  // [32][R] c_j K[j][m]
+  static constexpr int CFR = PR + 32 * R * 4;               // [TPL_CFR] final coefficients
+  static constexpr int STAG = CFR + TPL_CFR * 4;            // [TPL_STG] stage tags
   static constexpr int RED = STAG + TPL_STG * 4;            // nact, status
-  static constexpr int TKB = RED + 16;                      // [64] mbarriers: m taken over
-  static constexpr int STG = TKB + 64 * 8;                  // [TPL_STG][SSTR] stages
-  static constexpr int CFIN = STG + TPL_STG * SSTR * 4;     // [Np] final coefficients
-  static size_t bytes(int Np) { return (size_t)CFIN + (size_t)Np * 4; }
+  static constexpr int TKB = RED + 16;                      // [32] mbarriers: m taken over
+  static constexpr int STG = TKB + 32 * 8;                  // [TPL_STG][SSTR] stages
+  static constexpr int TOTAL = STG + TPL_STG * SSTR * 4;
 };
 __host__ __device__ constexpr int tpl_kpl(int M) { return (M + 31) / 32; }
+__host__ __device__ constexpr int tpl_span(int NW, int W) { return NW == 1 ? TP_SPAN : W + 7; }
+template <int NW>
+static size_t tpl_bytes(int M) {
+  return tpl_kpl(M) == 1 ? (size_t)TplL<1, NW>::TOTAL : (size_t)TplL<2, NW>::TOTAL;
+}
 
-template <int KPL>
-__global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
+template <int KPL, int NW>
+__global__ void __launch_bounds__(32 * (NW + TPL_NH), 1)
     apsm_train_tpl_kernel(const float* __restrict__ rx, long long rx_stride,
                           const float* __restrict__ targets, const float* __restrict__ kband,
                           const unsigned* __restrict__ plive, const int* __restrict__ pcnt,
@@ -916,26 +923,31 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
                           int* __restrict__ fs_out, float* __restrict__ theta_out,
                           int* __restrict__ nact_out, int* __restrict__ status_out) {
   extern __shared__ __align__(128) unsigned char smem_tp[];
-  using L = TplL<KPL>;
-  constexpr int XR = L::XR, SSTR = L::SSTR, OKB = L::OKB, OLV = L::OLV, OB = L::OB,
-                OLC = L::OLC;
-  const int Np = 2 * n_train, D = 2 * M, P = tp_lead(W);
+  using L = TplL<KPL, NW>;
+  constexpr int R = L::R, KS = L::KS, XR = L::XR, SSTR = L::SSTR;
+  constexpr int OLR = L::OLR, OKB = L::OKB, OLV = L::OLV, OB = L::OB, OLC = L::OLC;
+  constexpr int NT = 32 * (NW + TPL_NH);
+  // takeover lead P: the one-warp ring keeps K2t's P = 28 - W; wider rings
+  // take over 7 steps ahead (P < 32: the init / p / mbarrier rings are 32 deep)
+  const int SPAN = tpl_span(NW, W);
+  const int Np = 2 * n_train, D = 2 * M, P = SPAN - W;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x;
   if (task >= F * K) return;
   const unsigned sb = smem_u32(smem_tp);
-  float* Ks = reinterpret_cast<float*>(smem_tp + L::KS);
+  float* Ks = reinterpret_cast<float*>(smem_tp + L::KSO);
   float* dsm = reinterpret_cast<float*>(smem_tp + L::DSM);
   float* qs = reinterpret_cast<float*>(smem_tp + L::QS);
+  float* prg = reinterpret_cast<float*>(smem_tp + L::PR);
+  float* cfr = reinterpret_cast<float*>(smem_tp + L::CFR);
   int* stag = reinterpret_cast<int*>(smem_tp + L::STAG);
   int* red = reinterpret_cast<int*>(smem_tp + L::RED);
   const float* Sg = reinterpret_cast<const float*>(smem_tp + L::STG);
-  float* cfin = reinterpret_cast<float*>(smem_tp + L::CFIN);
-  const unsigned s_init = sb + L::INIT, s_pr = sb + L::PR;
+  const unsigned s_init = sb + L::INIT, s_tkb = sb + L::TKB;
   const int f = task / K;
   const float* X = rx + (long long)f * rx_stride;
   const float* Bt = targets + (long long)task * Np;
-  const float* KB = kband + (long long)f * Np * 32;
+  const float* KB = kband + (long long)f * Np * R;
   const int NWp = (n_train + 31) / 32;
   const unsigned* LW = plive + (long long)f * NWp * n_train;
   const int* LC = pcnt + (long long)f * n_train;
@@ -944,45 +956,47 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
   int* FSout = fs_out + (long long)task * Np;
   const bool gauss = w_g != 0.f;
 
-  for (int i = threadIdx.x; i < TP_RING * TP_KS; i += blockDim.x) Ks[i] = 0.f;
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
-    dsm[i] = 0.f;
-    st_tag(s_init + 8u * i, 0.f, -1);
-  }
-  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) st_tag(s_pr + 8u * i, 0.f, -1);
-  for (int i = threadIdx.x; i < TPL_STG; i += blockDim.x) stag[i] = -1;
-  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+  for (int i = threadIdx.x; i < R * KS; i += NT) Ks[i] = 0.f;
+  for (int i = threadIdx.x; i < 2 * R; i += NT) dsm[i] = 0.f;
+  for (int i = threadIdx.x; i < 32; i += NT) st_tag(s_init + 8u * i, 0.f, -1);
+  for (int i = threadIdx.x; i < TPL_STG; i += NT) stag[i] = -1;
+  for (int i = threadIdx.x; i < W; i += NT) {
     qs[2 * i] = qtab ? qtab[2 * i] : 1.f / (float)(i + 1);
     qs[2 * i + 1] = qtab ? qtab[2 * i + 1] : 1.f / (float)(i + 1);
   }
   if (threadIdx.x == 0) {
     red[0] = red[1] = 0;
-    for (int i = 0; i < 64; ++i)
+    for (int i = 0; i < 32; ++i)
       mbar_init(reinterpret_cast<unsigned long long*>(smem_tp + L::TKB) + i, 1);
     mbar_fence_init();
   }
   __syncthreads();
-  const unsigned s_tkb = sb + L::TKB;
 
-  if (warp == 0) {
-    // ================= critical warp =================
+  if (warp < NW) {
+    // ================= ring warps =================
     // steps as straight-line code (takeover / delta parts selected at compile
-    // time for the warm-up, main and tail ranges); the tags it depends on are
-    // loaded at the top of a step and tested at its end: the init of the sample
-    // entering next, and the stage TPL_LA samples ahead of the takeover
+    // time for the warm-up, window-filling, main and tail ranges); the tags a
+    // step depends on are tested after its deltas are out
     constexpr int TPL_LA = 2;
+    const int j = threadIdx.x;                   // my slot
     float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
     int samp = -(1 << 30), fs = -1, nact = 0, status = 0;
-    const unsigned krow = sb + L::KS + (unsigned)(lane * TP_KS) * 4;
-    const unsigned dsa = sb + L::DSM;
     const float qmc = qs[2 * (W - 1)], qlc = qs[2 * (W - 1) + 1];
+    const float4* kk4 = reinterpret_cast<const float4*>(Ks + j * KS);
     for (int s = 0; s < TPL_LA && s < Np; ++s)
       while (ld_volatile(stag + s) != s) {
       }
+    int sm = 0;                                  // slot of m = n + P   (mod R)
+    int sn = (R - P % R) % R;                    // slot of n
+    auto ring_sync = [&]() {
+      if constexpr (NW == 1) __syncwarp();
+      else named_bar(2, 32 * NW);
+    };
     auto step = [&](const int n, auto tk, auto dl_on, auto qconst) {
       const int m = n + P, e = n + 1, a = n - W + 1;
+      float* dcur = dsm + (NW == 1 ? 0 : (n & 1) * R);
       // ---- step n: my slot's delta (the critical chain starts here) ----
-      float c_prev = c;
+      const float c_prev = c;
       if constexpr (decltype(dl_on)::value) {
         const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
         float qm, ql;
@@ -999,10 +1013,8 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
         dl = inw ? dl : 0.f;
         c += dl;
         fs = (dl != 0.f && fs < 0) ? n : fs;
-        dsm[lane] = dl;
+        dcur[j] = dl;
       }
-      // tags this step depends on: the init of the sample entering at step e,
-      // and the stage TPL_LA samples ahead of the takeover
       float iv;
       int itag;
       ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
@@ -1010,16 +1022,17 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
       const int sgtag = ld_volatile(stag + (la & (TPL_STG - 1)));
       bool mine = false;
       if constexpr (decltype(tk)::value) {       // ---- takeover of sample m ----
-        const int sm = m & 31;
         const float* sg = Sg + (m & (TPL_STG - 1)) * SSTR;
-        const float v = sg[OKB + ((sm - lane) & 31)];      // K[m][this lane's sample]
-        Ks[sm * TP_KS + lane] = v;
-        Ks[lane * TP_KS + sm] = v;
+        int d = sm - j;                          // m - (the sample in my slot)
+        d += d < 0 ? R : 0;
+        const float v = sg[OKB + d];             // K[m][my sample]
+        Ks[sm * KS + j] = v;
+        Ks[j * KS + sm] = v;
         // c_j K[j][m] of the window [n-W+1, n-1] before step n's deltas
         const bool win = (unsigned)(samp - (n - W + 1)) < (unsigned)(W - 1);
-        st_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), win ? c_prev * v : 0.f, m);
+        prg[(m & 31) * R + j] = win ? c_prev * v : 0.f;
         const float b = sg[OB];
-        mine = lane == sm;
+        mine = j == sm;
         samp = mine ? m : samp;
         c = mine ? 0.f : c;
         fs = mine ? -1 : fs;
@@ -1030,36 +1043,66 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
         bl = mine ? b - eps : bl;
         bh = mine ? b + eps : bh;
       }
-      __syncwarp();                              // deltas and the takeover's K row/column
+      ring_sync();                               // deltas and the takeover's K row/column
       if constexpr (decltype(tk)::value) {       // m taken over: wake its helper
-        if (lane == 0)
+        if (j == 0)
           asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];"
-                       ::"r"(s_tkb + 8u * (unsigned)(m & 63)) : "memory");
+                       ::"r"(s_tkb + 8u * (unsigned)(m & 31)) : "memory");
       }
       if (e >= 0 && e < Np && __any_sync(0xffffffffu, itag != e)) {
         do {                                     // (a helper is late: rare)
           ld_tagged(s_init + 8u * (unsigned)(e & 31), iv, itag);
         } while (__any_sync(0xffffffffu, itag != e));
       }
-      const float add = (e >= 0 && e < Np && lane == (e & 31)) ? iv : 0.f;
+      int se = sn + 1;
+      se -= se >= R ? R : 0;                     // slot of e
+      const float add = (e >= 0 && e < Np && j == se) ? iv : 0.f;
       if constexpr (decltype(dl_on)::value) {
+        const float4* dd4 = reinterpret_cast<const float4*>(dcur);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        if constexpr (NW == 1) {
 #pragma unroll
-        for (int s = 0; s < 32; s += 8) {
-          const float4 d0 = lds_f4(dsa + 4u * s), k0 = lds_f4(krow + 4u * s);
-          const float4 d1 = lds_f4(dsa + 4u * (s + 4)), k1 = lds_f4(krow + 4u * (s + 4));
-          a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
-          a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
-          a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
-          a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+          for (int s = 0; s < 8; s += 2) {
+            const float4 d0 = dd4[s], k0 = kk4[s], d1 = dd4[s + 1], k1 = kk4[s + 1];
+            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+            a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+            a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+          }
+        } else {                                 // the window's 4-slot chunks
+          const int lo = n - W + 1 > 0 ? n - W + 1 : 0;
+          int slo = sn - (n - lo);
+          slo += slo < 0 ? R : 0;
+          const int c0 = slo >> 2, nch = (n >> 2) - (lo >> 2) + 1;
+          const int e1 = c0 + nch < R / 4 ? c0 + nch : R / 4;
+          auto chunk2 = [&](int k) {
+            const float4 d0 = dd4[k], k0 = kk4[k], d1 = dd4[k + 1], k1 = kk4[k + 1];
+            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+            a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+            a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+          };
+          auto chunk1 = [&](int k) {
+            const float4 d0 = dd4[k], k0 = kk4[k];
+            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+          };
+          int k = c0;
+          for (; k + 1 < e1; k += 2) chunk2(k);
+          if (k < e1) chunk1(k);
+          const int rest = nch - (e1 - c0);
+          for (k = 0; k + 1 < rest; k += 2) chunk2(k);
+          if (k < rest) chunk1(k);
         }
         const float upd = ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
         Y = (mine ? 0.f : Y) + (upd + add);      // the taken-over slot restarts at 0
       } else {
         Y = (mine ? 0.f : Y) + add;
       }
-      const bool own = a >= 0 && lane == (a & 31);   // leaves after this step: c is final
-      if (own) cfin[a] = c;
+      int sa = sn - (W - 1);
+      sa += sa < 0 ? R : 0;                      // slot of a
+      const bool own = a >= 0 && j == sa;        // leaves after this step: c is final
+      if (own) cfr[a & (TPL_CFR - 1)] = c;
       stg_if(own, Cout + a, c);
       stg_if(own, FSout + a, fs);
       nact += (own && fs >= 0) ? 1 : 0;
@@ -1067,7 +1110,9 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
         while (ld_volatile(stag + (la & (TPL_STG - 1))) != la) {
         }
       }
-      __syncwarp();                              // delta reads done before the next writes
+      if constexpr (NW == 1) __syncwarp();       // delta reads done before the next writes
+      sm = sm + 1 == R ? 0 : sm + 1;
+      sn = se;
     };
     using T_ = std::true_type;
     using F_ = std::false_type;
@@ -1078,62 +1123,56 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
     for (; n < 0; ++n) step(n, F_{}, F_{}, F_{});                           // (Np <= P)
     for (; n < Np; ++n) step(n, F_{}, T_{}, F_{});                          // tail: no takeover
     if (samp >= 0 && samp < Np && samp > Np - W) {   // still in the window after the last step
-      cfin[samp] = c;
       Cout[samp] = c;
       FSout[samp] = fs;
       nact += fs >= 0;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      nact += __shfl_xor_sync(0xffffffffu, nact, o);
-      status |= __shfl_xor_sync(0xffffffffu, status, o);
-    }
-    if (lane == 0) {
-      red[0] = nact;
-      red[1] = status;
-    }
-    named_bar(1, 32 * (1 + TPL_NH));
+    atomicAdd(&red[0], nact);
+    atomicOr(&red[1], status);
+    named_bar(1, NT);
   } else {
     // ================= helper warps =================
-    const int h = warp - 1;
+    const int h = warp - NW;
     const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
-    const int XP = vec ? D / 4 : D, NPC = XP + 18;
+    const int XP = vec ? D / 4 : D, NPC = 2 * XP + R / 4 + 10;
     const unsigned sg_s = sb + L::STG;
-    // stage of sample s: pilot row, band row, live list, target, live count;
-    // lane piece r (<= 5 per lane): shared offset, size, global address
-    // g + s * gs + (s >> 1) * gt
-    constexpr int PR_MAX = (2 * 64 * KPL + 18 + 31) / 32;
+    // stage of sample s: pilot rows of s and of s - SPAN + 1, band row, live
+    // list, target, live count; lane piece r: shared offset, size, global
+    // address g + mm * gs + (mm >> 1) * gt for the piece's sample mm = s - off
+    constexpr int PR_MAX = (2 * 64 * KPL + 32 * NW / 4 + 10 + 31) / 32;
     const char* pg[PR_MAX];
-    int pgs[PR_MAX], pgt[PR_MAX];
+    int pgs[PR_MAX], pgt[PR_MAX], pof[PR_MAX], psz[PR_MAX];
     unsigned pso[PR_MAX];
-    int psz[PR_MAX];
 #pragma unroll
     for (int r = 0; r < PR_MAX; ++r) {
-      const int pc = lane + 32 * r;
-      pg[r] = nullptr; pgs[r] = 0; pgt[r] = 0; pso[r] = 0; psz[r] = 0;
-      if (pc < XP) {
+      int pc = lane + 32 * r;
+      pg[r] = nullptr; pgs[r] = 0; pgt[r] = 0; pso[r] = 0; psz[r] = 0; pof[r] = 0;
+      if (pc < 2 * XP) {
+        const int lv = pc >= XP;
+        if (lv) pc -= XP;
         pg[r] = reinterpret_cast<const char*>(X + (vec ? 4 * pc : pc));
         pgt[r] = D * 4;
-        pso[r] = (unsigned)(vec ? 16 * pc : 4 * pc);
+        pso[r] = (unsigned)(lv * OLR + (vec ? 4 * pc : pc)) * 4;
         psz[r] = vec ? 16 : 4;
-      } else if (pc < XP + 8) {
-        const int q = pc - XP;
+        pof[r] = lv ? SPAN - 1 : 0;
+      } else if (pc < 2 * XP + R / 4) {
+        const int q = pc - 2 * XP;
         pg[r] = reinterpret_cast<const char*>(KB + 4 * q);
-        pgs[r] = 128;
+        pgs[r] = R * 4;
         pso[r] = (unsigned)(OKB + 4 * q) * 4;
         psz[r] = 16;
-      } else if (pc < XP + 16) {
-        const int q = pc - XP - 8;
+      } else if (pc < 2 * XP + R / 4 + 8) {
+        const int q = pc - 2 * XP - R / 4;
         pg[r] = reinterpret_cast<const char*>(LV + q);
         pgt[r] = TP_CAP * 16;
         pso[r] = (unsigned)(OLV + 4 * q) * 4;
         psz[r] = gauss ? 16 : 0;
-      } else if (pc == XP + 16) {
+      } else if (pc == 2 * XP + R / 4 + 8) {
         pg[r] = reinterpret_cast<const char*>(Bt);
         pgs[r] = 4;
         pso[r] = (unsigned)OB * 4;
         psz[r] = 4;
-      } else if (pc == XP + 17) {
+      } else if (pc == 2 * XP + R / 4 + 9) {
         pg[r] = reinterpret_cast<const char*>(LC);
         pgt[r] = 4;
         pso[r] = (unsigned)OLC * 4;
@@ -1143,18 +1182,19 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
     const int nr = (NPC + 31) / 32;
     auto prefetch = [&](int s) {
       const unsigned so = sg_s + (unsigned)((s & (TPL_STG - 1)) * SSTR) * 4;
-      const bool in = s < Np;
 #pragma unroll
       for (int r = 0; r < PR_MAX; ++r) {
         if (r < nr) {
-          const char* g = pg[r] + (long long)s * pgs[r] + (long long)(s >> 1) * pgt[r];
+          const int mm = s - pof[r];
+          const bool in = s < Np && mm >= 0;
+          const char* g = pg[r] + (long long)mm * pgs[r] + (long long)(mm >> 1) * pgt[r];
           cpa16_if(in && psz[r] == 16, so + pso[r], g);
           cpa4_if(in && psz[r] == 4, so + pso[r], g);
         }
       }
       cp_async_commit();
     };
-    for (int j = 0; j < TPL_J; ++j) prefetch(h + TPL_NH * j);
+    for (int jj = 0; jj < TPL_J; ++jj) prefetch(h + TPL_NH * jj);
     cp_async_wait<TPL_J - 2>();                 // my stages of h and h + NH landed
     __syncwarp();
     __threadfence_block();
@@ -1172,25 +1212,24 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
       __threadfence_block();
       if (lane == 0 && m + 2 * TPL_NH < Np)
         st_volatile(stag + ((m + 2 * TPL_NH) & (TPL_STG - 1)), m + 2 * TPL_NH);
-      // wait (suspended, not polling: no issue slots or shared-memory traffic
-      // taken from the critical warp) for m's takeover, then c_j K[j][m]
-      while (!mbar_try_wait_s(s_tkb + 8u * (unsigned)(m & 63), (unsigned)((m >> 6) & 1))) {
+      // wait (suspended in hardware: no issue slots or shared-memory traffic
+      // taken from the ring warps) for m's takeover
+      while (!mbar_try_wait_s(s_tkb + 8u * (unsigned)(m & 31), (unsigned)((m >> 5) & 1))) {
       }
-      float pv;
-      while (!ld_tag(s_pr + 8u * (unsigned)((m & 63) * 32 + lane), m, pv)) {
-      }
-      __syncwarp();
-      // theta_fin: the samples a <= m - SPAN (left the window by m's takeover)
-      // (pairs of samples: 2t and 2t + 1 share the pilot row of t; a sample a
-      // adds c_a r1(x) (a even) or c_a r2(x) (a odd), r1 = [Re; Im],
-      // r2 = [Im; -Re], apsm.py:156-169)
-      for (; next_a <= m - TP_SPAN; ++next_a) {
+      float part = 0.f;
+#pragma unroll
+      for (int i = 0; i < NW; ++i) part += prg[(m & 31) * R + lane + 32 * i];
+      // theta_fin: the samples a <= m - SPAN (left the window by m's takeover);
+      // the row of a is the leaving row of stage a + SPAN - 1.  (Samples 2t
+      // and 2t + 1 share the pilot row of t; a adds c_a r1(x) (a even) or
+      // c_a r2(x) (a odd), r1 = [Re; Im], r2 = [Im; -Re], apsm.py:156-169.)
+      for (; next_a <= m - SPAN; ++next_a) {
         const int a = next_a;
-        const float ca = cfin[a];
-        const bool pair = (a & 1) == 0 && a + 1 <= m - TP_SPAN;
-        const float cb = pair ? cfin[a + 1] : 0.f;
+        const float ca = cfr[a & (TPL_CFR - 1)];
+        const bool pair = (a & 1) == 0 && a + 1 <= m - SPAN;
+        const float cb = pair ? cfr[(a + 1) & (TPL_CFR - 1)] : 0.f;
         const float ce = (a & 1) ? 0.f : ca, co = (a & 1) ? ca : cb;
-        const float* xa = Sg + (a & (TPL_STG - 1)) * SSTR;
+        const float* xa = Sg + ((a + SPAN - 1) & (TPL_STG - 1)) * SSTR + OLR;
 #pragma unroll
         for (int i = 0; i < KPL; ++i) {
           const int k = lane + 32 * i;
@@ -1203,15 +1242,15 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
         next_a += pair ? 1 : 0;
       }
       const float* sm_ = Sg + (m & (TPL_STG - 1)) * SSTR;
-      float part = pv, lin = 0.f;
+      float lin = 0.f;
       const int bt = m & 1;
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int k = lane + 32 * i;
         if (k < M) {
-          const float xr = sm_[2 * k], xi = sm_[2 * k + 1];
-          lin = fmaf(th[i].x, bt ? xi : xr, lin);
-          lin = fmaf(th[i].y, bt ? -xr : xi, lin);
+          const float2 x = *reinterpret_cast<const float2*>(sm_ + 2 * k);
+          lin = fmaf(th[i].x, bt ? x.y : x.x, lin);
+          lin = fmaf(th[i].y, bt ? -x.x : x.y, lin);
         }
       }
       part = fmaf(w_l, lin, part);
@@ -1221,9 +1260,9 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
           if (lane < 2 * cnt) {
             const float4 v4 = reinterpret_cast<const float4*>(sm_ + OLV)[lane >> 1];
             const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
-            if (a <= m - TP_SPAN) {
+            if (a <= m - SPAN) {
               const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
-              part = fmaf(w_g * cfin[a], kap, part);
+              part = fmaf(w_g * __ldcg(Cout + a), kap, part);
             }
           }
         } else if (cnt < 0) {                   // more live pilots than the list holds
@@ -1237,13 +1276,13 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
               const float* xa = X + (long long)p * D;
               for (int al = 0; al < 2; ++al) {
                 const int a = 2 * p + al;
-                if (a > m - TP_SPAN) continue;
+                if (a > m - SPAN) continue;
                 float dist = 0.f;
                 for (int e2 = 0; e2 < D; ++e2) {
                   const float z = rcomp(xa, e2, al) - rcomp(xm, e2, bt);
                   dist = fmaf(z, z, dist);
                 }
-                part = fmaf(w_g * cfin[a], exp_fast(-dist * inv2s), part);
+                part = fmaf(w_g * __ldcg(Cout + a), exp_fast(-dist * inv2s), part);
               }
             }
           }
@@ -1253,11 +1292,11 @@ __global__ void __launch_bounds__(32 * (1 + TPL_NH), 1)
       if (lane == 0) st_tag(s_init + 8u * (unsigned)(m & 31), init, m);
     }
     cp_async_wait<0>();
-    named_bar(1, 32 * (1 + TPL_NH));
+    named_bar(1, NT);
     if (h == 0) {                               // theta = w_l (all final c_a r_a)
       for (; next_a < Np; ++next_a) {
         const int a = next_a;
-        const float ca = cfin[a];
+        const float ca = __ldcg(Cout + a);
         const float* xa = X + (long long)(a >> 1) * D;
 #pragma unroll
         for (int i = 0; i < KPL; ++i) {
@@ -1346,20 +1385,31 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
                                      kband, R);
     if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
   }
+  const int tasks = F * K;
+  // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
+  // so no other CTA (the concurrent detection screen) shares its SM, and the
+  // ring-warps + helpers form when its shared memory fits
+  const bool lat = tasks <= tp_num_sms();
+  const int NWr = R / 32, KPL = tpl_kpl(M);
+  size_t tpl_smem = 0;
+  switch (NWr) {
+    case 1: tpl_smem = tpl_bytes<1>(M); break;
+    case 2: tpl_smem = tpl_bytes<2>(M); break;
+    case 3: tpl_smem = tpl_bytes<3>(M); break;
+    case 4: tpl_smem = tpl_bytes<4>(M); break;
+    default: tpl_smem = tpl_bytes<5>(M); break;
+  }
+  const bool tpl = lat && !(stages & 8) && tpl_smem <= 227 * 1024;
+  const int span = tpl ? tpl_span(NWr, W) : SPAN;
   if ((stages & 2) && p.w_g != 0.0) {
-    // lists only hold pilots p <= t - SPAN / 2 of row t: the trainer's live
-    // terms are the samples a <= m - SPAN (the band rows cover the rest)
-    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, -(SPAN / 2), M, p,
+    // lists only hold pilots p <= t - span / 2 of row t: the trainer's live
+    // terms are the samples a <= m - span (the band rows cover the rest)
+    const int r = screen_tc_rows(rx, rx_stride, F, n_train, n_train, 0, -(span / 2), M, p,
                                  plive, pcnt, pvals, s);
     if (r) return r;
   }
   if (!(stages & 4)) return KAPSM_OK;
-  const int tasks = F * K;
   const int DPL = (2 * M + 31) / 32;
-  // latency (chains <= SMs): one chain per CTA with >= 120 KB of shared memory,
-  // so no other CTA (the concurrent detection screen) shares its SM;
-  // throughput: 4 chains per CTA (several CTAs per SM)
-  const bool lat = tasks <= tp_num_sms();
   auto launch = [&](auto kern, int wpc, int threads, size_t smem) -> int {
     if (lat && smem < 120 * 1024) smem = 120 * 1024;
     if (smem > 227 * 1024) return (int)KAPSM_ERR_UNSUPPORTED;
@@ -1371,16 +1421,19 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
         (float)p.w_l, (float)p.w_g, inv2s, qtab, coeff, first_step, theta, n_active, status);
     return status_from(cudaGetLastError());
   };
-  // latency mode: the critical-warp + helpers form (stages bit 8: the plain
-  // one-warp form instead, for A/B tests)
-  const int Np2 = 2 * n_train;
-  if (R == TP_RING && lat && !(stages & 8) && Np2 <= TPL_MAXNP) {
-    const int KPL = tpl_kpl(M);
-    const size_t smem = KPL == 1 ? TplL<1>::bytes(Np2) : TplL<2>::bytes(Np2);
-    if (smem <= 227 * 1024) {
-      if (KPL == 1) return launch(apsm_train_tpl_kernel<1>, 1, 32 * (1 + TPL_NH), smem);
-      return launch(apsm_train_tpl_kernel<2>, 1, 32 * (1 + TPL_NH), smem);
-    }
+  if (tpl) {                                   // latency: ring warps + helpers
+    const size_t smem = tpl_smem;
+#define KAPSM_TPL(NWV)                                                                        \
+  if (NWr == NWV) {                                                                           \
+    if (KPL == 1) return launch(apsm_train_tpl_kernel<1, NWV>, 1, 32 * (NWV + TPL_NH), smem); \
+    return launch(apsm_train_tpl_kernel<2, NWV>, 1, 32 * (NWV + TPL_NH), smem);               \
+  }
+    KAPSM_TPL(1)
+    KAPSM_TPL(2)
+    KAPSM_TPL(3)
+    KAPSM_TPL(4)
+    KAPSM_TPL(5)
+#undef KAPSM_TPL
   }
   if (R == TP_RING) {
     int wpc = lat ? 1 : 4;
