@@ -1060,39 +1060,18 @@ __global__ void __launch_bounds__(32 * (NW + TPL_NH), 1)
       if constexpr (decltype(dl_on)::value) {
         const float4* dd4 = reinterpret_cast<const float4*>(dcur);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-        if constexpr (NW == 1) {
+        {
+          // the whole ring, unrolled and branch-free (deltas outside the
+          // window are zero, K is finite everywhere): every load can be in
+          // flight at once, at (R - W - P) / R extra shared-memory traffic
 #pragma unroll
-          for (int s = 0; s < 8; s += 2) {
-            const float4 d0 = dd4[s], k0 = kk4[s], d1 = dd4[s + 1], k1 = kk4[s + 1];
-            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
-            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
-            a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
-            a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
-          }
-        } else {                                 // the window's 4-slot chunks
-          const int lo = n - W + 1 > 0 ? n - W + 1 : 0;
-          int slo = sn - (n - lo);
-          slo += slo < 0 ? R : 0;
-          const int c0 = slo >> 2, nch = (n >> 2) - (lo >> 2) + 1;
-          const int e1 = c0 + nch < R / 4 ? c0 + nch : R / 4;
-          auto chunk2 = [&](int k) {
+          for (int k = 0; k < R / 4; k += 2) {
             const float4 d0 = dd4[k], k0 = kk4[k], d1 = dd4[k + 1], k1 = kk4[k + 1];
             a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
             a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
             a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
             a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
-          };
-          auto chunk1 = [&](int k) {
-            const float4 d0 = dd4[k], k0 = kk4[k];
-            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
-            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
-          };
-          int k = c0;
-          for (; k + 1 < e1; k += 2) chunk2(k);
-          if (k < e1) chunk1(k);
-          const int rest = nch - (e1 - c0);
-          for (k = 0; k + 1 < rest; k += 2) chunk2(k);
-          if (k < rest) chunk1(k);
+          }
         }
         const float upd = ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
         Y = (mine ? 0.f : Y) + (upd + add);      // the taken-over slot restarts at 0
