@@ -170,6 +170,17 @@ KAPSM_DEV float warp_sum_f(float v) {
   return v;
 }
 
+KAPSM_DEV float2 ffma2(float2 a, float2 b, float2 c) {     // packed FP32x2 FMA (FFMA2)
+  unsigned long long ra, rb, rc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rc) : "l"(ra), "l"(rb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(rc));
+  return r;
+}
+
 // realified component e of sample (beta) from its interleaved pilot row x
 KAPSM_DEV float rcomp(const float* x, int e, int beta) {
   if (!beta) return x[e];
@@ -220,20 +231,15 @@ __global__ void __launch_bounds__(128, 6)
   }
   dsm[lane] = 0.f;
 
-  // prefetch pieces of sample m into stage m mod STG (one cp.async group per
-  // step): the pilot row (16-byte pieces, or 4-byte ones when rows are not
-  // 16-byte aligned), the band row and the live-list row (8 pieces each), the
-  // target and the row's live count.  Each lane owns up to two pieces for the
-  // whole chain: global address g + m * gm + (m >> 1) * gt, shared address
-  // s + (m mod STG) * SSTR * 4, size 16 or 4 bytes (0: none).
   // prefetch pieces into stage m mod STG (one cp.async group per step): the
   // pilot rows of sample m and of the leaving sample m - SPAN + 1 (16-byte
   // pieces, or 4-byte ones when rows are not 16-byte aligned), the band row
-  // and the live-list row (8 pieces each), the target and the row's live
-  // count.  A lane owns up to 3 pieces for the whole chain; each keeps a
-  // running global pointer for its sample mm (m or m - SPAN + 1):
-  // g + mm * gm + (mm >> 1) * gt, advanced by gm + (mm odd) gt per step.
-  const int XP = vec ? D / 4 : D, NPC = 2 * XP + 18;
+  // (8 pieces), the target and the row's live count (the live-list row itself
+  // is read from global memory in the rare steps whose count is nonzero).  A
+  // lane owns up to 3 pieces for the whole chain; each keeps a running global
+  // pointer for its sample mm (m or m - SPAN + 1): g + mm * gm + (mm >> 1) * gt,
+  // advanced by gm + (mm odd) gt per step.
+  const int XP = vec ? D / 4 : D, NPC = 2 * XP + 10;
   const unsigned sg_s = sbase + L::STG;
   const char* pp[3];
   long long pgm[3], pgt[3];
@@ -258,18 +264,12 @@ __global__ void __launch_bounds__(128, 6)
       pgm[r] = 128;
       ps[r] = sg_s + (unsigned)(OKB + 4 * q) * 4;
       psz[r] = 16;
-    } else if (pc < 2 * XP + 16) {
-      const int q = pc - 2 * XP - 8;
-      g = reinterpret_cast<const char*>(LV + q);
-      pgt[r] = (long long)TP_CAP * 16;
-      ps[r] = sg_s + (unsigned)(OLV + 4 * q) * 4;
-      psz[r] = gauss ? 16 : 0;
-    } else if (pc == 2 * XP + 16) {
+    } else if (pc == 2 * XP + 8) {
       g = reinterpret_cast<const char*>(Bt);
       pgm[r] = 4;
       ps[r] = sg_s + (unsigned)OB * 4;
       psz[r] = 4;
-    } else if (pc == 2 * XP + 17) {
+    } else if (pc == 2 * XP + 9) {
       g = reinterpret_cast<const char*>(LC);
       pgt[r] = 4;
       ps[r] = sg_s + (unsigned)OLC * 4;
@@ -303,71 +303,81 @@ __global__ void __launch_bounds__(128, 6)
   int samp = -(1 << 30);          // sample held by this lane's slot
   float Y = 0.f, c = 0.f, idn = 0.f, bl = 0.f, bh = 0.f;
   int fs = -1, nact = 0, status = 0;
-  float th[DPL];
+  // theta_fin as (Re, Im) pairs: lane k (+ 32 i) holds antenna k, i.e.
+  // components k and M + k of the reference's block layout [Re; Im]
+  constexpr int KPL = (DPL + 1) / 2;
+  float2 th[KPL];
 #pragma unroll
-  for (int i = 0; i < DPL; ++i) th[i] = 0.f;
+  for (int i = 0; i < KPL; ++i) th[i] = make_float2(0.f, 0.f);
+  const unsigned krow = sbase + L::KS + (unsigned)(lane * TP_KS) * 4;   // K[.][my sample]
+  const unsigned dsa = sbase + L::DSM;
+  const float qmc = qs[2 * (W - 1)], qlc = qs[2 * (W - 1) + 1];
 
-  for (int n = -P; n < Np; ++n) {
+  // one step; MAIN: n >= W - 1 and m = n + P < Np (every part present, q
+  // constant), compile-time so the steady state is straight-line code
+  auto step = [&](const int n, auto main_) {
+    constexpr bool MAIN = decltype(main_)::value;
     const int m = n + P;                        // taken over this step
     cp_async_wait<TP_AHEAD - 1>();              // m's stage (issued TP_AHEAD steps ago) landed
     __syncwarp();
     // ---- live Gaussian terms of sample ml = m - 2: older samples, final c ----
     const int ml = m - TP_LIVE_LAG;
-    if (gauss && ml >= 0 && ml < Np) {
+    if (gauss && (MAIN || (ml >= 0 && ml < Np))) {
       const float* sl = Sg + (ml & (TP_STG - 1)) * SSTR;
       const int cnt = __float_as_int(sl[OLC]);
-      const int bt = ml & 1;
-      float part = 0.f;
-      if (cnt > 0) {
-        if (lane < 2 * cnt) {
-          const float4 v4 = reinterpret_cast<const float4*>(sl + OLV)[lane >> 1];
-          const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
-          if (a <= ml - TP_SPAN) {
-            const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
-            part = w_g * __ldcg(Cout + a) * kap;
+      if (cnt != 0) {
+        const int bt = ml & 1;
+        float part = 0.f;
+        if (cnt > 0) {                          // the list row (rare: from global)
+          if (lane < 2 * cnt) {
+            const float4 v4 = __ldg(LV + (long long)(ml >> 1) * TP_CAP + (lane >> 1));
+            const int al = lane & 1, a = 2 * __float_as_int(v4.w) + al;
+            if (a <= ml - TP_SPAN) {
+              const float kap = al == 0 ? (bt == 0 ? v4.x : v4.y) : (bt == 0 ? v4.z : v4.x);
+              part = w_g * __ldcg(Cout + a) * kap;
+            }
           }
-        }
-      } else if (cnt < 0) {                     // more live pilots than the list holds
-        const int tl = ml >> 1;
-        const float* xm = X + (long long)tl * D;
-        for (int w = lane; w < NWp; w += 32) {
-          unsigned bits = LW[(long long)w * n_train + tl];
-          while (bits) {
-            const int p = w * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            const float* xa = X + (long long)p * D;
-            for (int al = 0; al < 2; ++al) {
-              const int a = 2 * p + al;
-              if (a > ml - TP_SPAN) continue;
-              float dist = 0.f;
-              for (int e = 0; e < D; ++e) {
-                const float z = rcomp(xa, e, al) - rcomp(xm, e, bt);
-                dist = fmaf(z, z, dist);
+        } else {                                // more live pilots than the list holds
+          const int tl = ml >> 1;
+          const float* xm = X + (long long)tl * D;
+          for (int w = lane; w < NWp; w += 32) {
+            unsigned bits = LW[(long long)w * n_train + tl];
+            while (bits) {
+              const int p = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const float* xa = X + (long long)p * D;
+              for (int al = 0; al < 2; ++al) {
+                const int a = 2 * p + al;
+                if (a > ml - TP_SPAN) continue;
+                float dist = 0.f;
+                for (int e = 0; e < D; ++e) {
+                  const float z = rcomp(xa, e, al) - rcomp(xm, e, bt);
+                  dist = fmaf(z, z, dist);
+                }
+                part = fmaf(w_g * __ldcg(Cout + a), exp_fast(-dist * inv2s), part);
               }
-              part = fmaf(w_g * __ldcg(Cout + a), exp_fast(-dist * inv2s), part);
             }
           }
         }
-      }
-      if (__any_sync(0xffffffffu, part != 0.f)) {
         part = warp_sum_f(part);
         if (lane == (ml & 31)) Y += part;
       }
     }
     // ---- takeover of sample m into slot sm ----
     const float* sg = Sg + (m & (TP_STG - 1)) * SSTR;     // this step's stage
-    if (m < Np) {
+    if (MAIN || m < Np) {
       const int sm = m & 31, bt = m & 1;
       const float v = sg[OKB + ((sm - lane) & 31)];        // K[m][this lane's sample]
       Ks[sm * TP_KS + lane] = v;                           // K is symmetric: row and column
       Ks[lane * TP_KS + sm] = v;
       float pf = 0.f;
 #pragma unroll
-      for (int i = 0; i < DPL; ++i) {
-        const int e = lane + 32 * i;
-        if (e < D) {
-          const float x0 = sg[e], x1 = sg[e ^ 1];
-          pf = fmaf(th[i], bt ? ((e & 1) ? -x1 : x1) : x0, pf);
+      for (int i = 0; i < KPL; ++i) {
+        const int k = lane + 32 * i;
+        if (k < M) {                            // r1 = [Re; Im], r2 = [Im; -Re] (apsm.py:156-169)
+          const float2 x = *reinterpret_cast<const float2*>(sg + 2 * k);
+          pf = fmaf(th[i].x, bt ? x.y : x.x, pf);
+          pf = fmaf(th[i].y, bt ? -x.x : x.y, pf);
         }
       }
       pf *= w_l;
@@ -381,7 +391,8 @@ __global__ void __launch_bounds__(128, 6)
       c = mine ? 0.f : c;
       fs = mine ? -1 : fs;
       status |= (mine && !(v > 0.f)) ? (int)KAPSM_TRAIN_DEGENERATE : 0;   // kappa(r, r) = K[m][m]
-      const float rv = __fdividef(1.f, v);     // MUFU (the FP32 path's tolerance is 1e-4)
+      float rv;                                 // MUFU on every lane (tolerance 1e-4), no branch
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"(v));
       idn = mine ? (v > 0.f ? rv : 0.f) : idn;
       bl = mine ? b - eps : bl;
       bh = mine ? b + eps : bh;
@@ -389,10 +400,14 @@ __global__ void __launch_bounds__(128, 6)
     __syncwarp();                               // stage reads done before it is refilled
     prefetch();                                 // sample m + TP_AHEAD
     cp_async_commit();
-    if (n < 0) continue;
+    if (!MAIN && n < 0) return;
     // ---- step n: the window's deltas, then the window update ----
     const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
-    const float qm = qs[2 * cj], ql = qs[2 * cj + 1];
+    float qm = qmc, ql = qlc;
+    if (!MAIN) {
+      qm = qs[2 * cj];
+      ql = qs[2 * cj + 1];
+    }
     const float q = samp == n ? ql : qm;
     const bool inw = (unsigned)(samp - lo) <= (unsigned)cj;              // samp in [lo, n]
     float dl = q * idn * (fmaxf(bl - Y, 0.f) + fminf(bh - Y, 0.f));
@@ -401,30 +416,29 @@ __global__ void __launch_bounds__(128, 6)
     fs = (dl != 0.f && fs < 0) ? n : fs;
     dsm[lane] = dl;
     __syncwarp();                               // deltas and the takeover's K row/column
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    const unsigned krow = sbase + L::KS + (unsigned)(lane * TP_KS) * 4;   // K[.][my sample]
-    const unsigned dsa = sbase + L::DSM;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
-    for (int s = 0; s < 32; s += 4) {
-      const float4 dd = lds_f4(dsa + 4u * s);
-      const float4 kk = lds_f4(krow + 4u * s);
-      a0 = fmaf(dd.x, kk.x, a0);
-      a1 = fmaf(dd.y, kk.y, a1);
-      a2 = fmaf(dd.z, kk.z, a2);
-      a3 = fmaf(dd.w, kk.w, a3);
+    for (int s = 0; s < 32; s += 8) {
+      const float4 d0 = lds_f4(dsa + 4u * s), k0 = lds_f4(krow + 4u * s);
+      const float4 d1 = lds_f4(dsa + 4u * (s + 4)), k1 = lds_f4(krow + 4u * (s + 4));
+      a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+      a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+      a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+      a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
     }
-    Y += (a0 + a1) + (a2 + a3);
+    Y += ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
     // ---- the sample leaving after this step: its coefficient is final ----
     const int a = n - W + 1;                    // == m - TP_SPAN + 1: its row is in the stage
-    if (a >= 0) {
+    if (MAIN || a >= 0) {
       const float ca = __shfl_sync(0xffffffffu, c, a & 31);
-      const int ba = a & 1;
+      const bool odd = a & 1;
 #pragma unroll
-      for (int i = 0; i < DPL; ++i) {
-        const int e = lane + 32 * i;
-        if (e < D) {
-          const float x0 = sg[XR + e], x1 = sg[XR + (e ^ 1)];
-          th[i] = fmaf(ca, ba ? ((e & 1) ? -x1 : x1) : x0, th[i]);
+      for (int i = 0; i < KPL; ++i) {
+        const int k = lane + 32 * i;
+        if (k < M) {
+          const float2 x = *reinterpret_cast<const float2*>(sg + XR + 2 * k);
+          th[i].x = fmaf(ca, odd ? x.y : x.x, th[i].x);
+          th[i].y = fmaf(ca, odd ? -x.x : x.y, th[i].y);
         }
       }
       const bool own = lane == (a & 31);
@@ -432,7 +446,13 @@ __global__ void __launch_bounds__(128, 6)
       stg_if(own, FSout + a, fs);
       nact += (own && fs >= 0) ? 1 : 0;
     }
-  }
+  };
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  int n = -P;
+  for (; n < W - 1 && n < Np; ++n) step(n, F_{});
+  for (; n + P < Np; ++n) step(n, T_{});
+  for (; n < Np; ++n) step(n, F_{});
   cp_async_wait<0>();
   __syncwarp();
   // ---- samples still in the window after the last step (rows from global) ----
@@ -440,9 +460,13 @@ __global__ void __launch_bounds__(128, 6)
     const float ca = __shfl_sync(0xffffffffu, c, a & 31);
     const float* xa = X + (long long)(a >> 1) * D;
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) {
-      const int e = lane + 32 * i;
-      if (e < D) th[i] = fmaf(ca, rcomp(xa, e, a & 1), th[i]);
+    for (int i = 0; i < KPL; ++i) {
+      const int k = lane + 32 * i;
+      if (k < M) {
+        const float xr = xa[2 * k], xi = xa[2 * k + 1];
+        th[i].x = fmaf(ca, (a & 1) ? xi : xr, th[i].x);
+        th[i].y = fmaf(ca, (a & 1) ? -xr : xi, th[i].y);
+      }
     }
     if (lane == (a & 31)) {
       Cout[a] = c;
@@ -452,10 +476,12 @@ __global__ void __launch_bounds__(128, 6)
   }
   // theta = w_l theta_fin in the reference's block layout [Re; Im] (apsm.py:172-182)
 #pragma unroll
-  for (int i = 0; i < DPL; ++i) {
-    const int e = lane + 32 * i;
-    if (e < D)
-      theta_out[(long long)task * D + ((e & 1) ? M + (e >> 1) : (e >> 1))] = w_l * th[i];
+  for (int i = 0; i < KPL; ++i) {
+    const int k = lane + 32 * i;
+    if (k < M) {
+      theta_out[(long long)task * D + k] = w_l * th[i].x;
+      theta_out[(long long)task * D + M + k] = w_l * th[i].y;
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -517,16 +543,6 @@ static int tpw_total_rt(int NW, int M) {
   }
 }
 
-KAPSM_DEV float2 ffma2(float2 a, float2 b, float2 c) {     // packed FP32x2 FMA (FFMA2)
-  unsigned long long ra, rb, rc;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rc) : "l"(ra), "l"(rb));
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(rc));
-  return r;
-}
 
 template <int DPL, int NW>
 __global__ void __launch_bounds__(32 * NW, 1)
