@@ -214,10 +214,12 @@ __global__ void __launch_bounds__(SC_WARPS * 32)
 }
 
 // One thread per (payload symbol, user): linear part, the live pilots (their
-// words prefetched together), demap, counts.  Threads of the same payload
-// symbol share the live words and the pilot rows through L1; a CTA holds 32
-// symbols x up to 8 users (all users at the paper's K = 6: the payload rows
-// are staged once per frame), 4 users for the wide rows of M > 16.
+// words prefetched together), demap, counts.  A CTA holds up to 8 users (all
+// of a frame's at the paper's K = 6: the payload rows are staged once per
+// frame; 4 users for the wide rows of M > 16) and walks nb blocks of 32
+// symbols: theta is loaded once, and the next block's rows are loaded into
+// registers while the current block is finished (FP32, 16-byte rows), so a
+// CTA pays one memory latency instead of one per block.
 template <typename T, int MT>
 __global__ void __launch_bounds__(256)
     detect_finish_kernel(const T* __restrict__ rx, long long rx_stride, int K, int n_train,
@@ -228,171 +230,188 @@ __global__ void __launch_bounds__(256)
                          const unsigned* __restrict__ live, T* __restrict__ est_out,
                          unsigned char* __restrict__ labels_out,
                          unsigned long long* __restrict__ bit_err,
-                         unsigned long long* __restrict__ sym_err) {
+                         unsigned long long* __restrict__ sym_err, int nb) {
   __shared__ T pts[128];
-  // the CTA's 32 payload rows, staged with coalesced loads (one contiguous
-  // block of rx); odd row stride in (re, im) pairs: conflict-free pair reads
+  // 32 payload rows per buffer, two buffers; odd row stride in (re, im)
+  // pairs: conflict-free pair reads
   constexpr int YS = 2 * MT + 2;
-  __shared__ __align__(16) T ys[32 * YS];
+  constexpr int NBUF = sizeof(T) == 4 ? 2 : 1;             // FP64: one buffer (48 KB static)
+  __shared__ __align__(16) T ys[NBUF][32 * YS];
+  __shared__ __align__(16) T tvs[8][2 * MT];               // theta of the CTA's users
   const int f = blockIdx.z;
   const int lane = threadIdx.x;
   const int u = blockIdx.y * blockDim.y + threadIdx.y;
-  const int t = blockIdx.x * 32 + lane;
-  const bool tvalid = t < n_data;
   const int NW = (n_train + 31) / 32, Np = 2 * n_train;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int nthr = blockDim.x * blockDim.y;
+  const int rl = 2 * M;
   for (int i = tid; i < 2 * n_points; i += nthr) pts[i] = points[i];
   const T* Xf = rx + (long long)f * rx_stride;
-  {
-    const int t0 = blockIdx.x * 32, rows = min(32, n_data - t0), rl = 2 * M;
-    const T* src = Xf + (long long)(n_train + t0) * rl;
-    // all loads of a thread issued before its stores (one memory latency),
-    // 16-byte pieces of the 32 contiguous rows of rl = 2M elements
-    const int n = rows * rl;
-    if (sizeof(T) == 4 && (rl & 3) == 0 && ((size_t)src & 15) == 0) {
-      constexpr int PER = (32 * 2 * MT / 4 + 127) / 128;  // float4 per thread at >= 128 threads
-      const float4* s4 = reinterpret_cast<const float4*>(src);
-      float4 v[PER];
+  const int blk0 = blockIdx.x * nb;
+  const int nblk = min(nb, (n_data + 31) / 32 - blk0);
+  const T* src0 = Xf + (long long)(n_train + blk0 * 32) * rl;
+  const bool vec = sizeof(T) == 4 && (rl & 3) == 0 && ((size_t)src0 & 15) == 0 &&
+                   ((rx_stride & 3) == 0);
+  constexpr int PER = (32 * 2 * MT / 4 + 127) / 128;        // float4 per thread at >= 128 threads
+  float4 v[PER];
+  auto rows_of = [&](int b) { return min(32, n_data - (blk0 + b) * 32); };
+  auto load_regs = [&](int b) {                             // FP32 16-byte path
+    const float4* s4 = reinterpret_cast<const float4*>(src0 + (long long)b * 32 * rl);
+    const int n = rows_of(b) * rl;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int e4 = tid + i * nthr;
-        v[i] = 4 * e4 < n ? __ldg(s4 + e4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    for (int i = 0; i < PER; ++i) {
+      const int e4 = tid + i * nthr;
+      v[i] = 4 * e4 < n ? __ldg(s4 + e4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto store_regs = [&](int b, T* buf) {
+    const int n = rows_of(b) * rl;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int e = 4 * (tid + i * nthr);
-        if (e < n) {
-          const int r = e / rl, c = e - r * rl;
-          T* d = ys + r * YS + c;
-          d[0] = (T)v[i].x; d[1] = (T)v[i].y; d[2] = (T)v[i].z; d[3] = (T)v[i].w;
-        }
-      }
-      for (int e = 4 * (tid + PER * nthr); e < n; e += 4 * nthr) {   // (< 128 threads)
+    for (int i = 0; i < PER; ++i) {
+      const int e = 4 * (tid + i * nthr);
+      if (e < n) {
         const int r = e / rl, c = e - r * rl;
-        for (int j = 0; j < 4; ++j) ys[r * YS + c + j] = src[e + j];
-      }
-    } else {
-      for (int e = tid; e < n; e += nthr) {
-        const int r = e / rl;
-        ys[r * YS + (e - r * rl)] = src[e];
+        T* d = buf + r * YS + c;
+        d[0] = (T)v[i].x; d[1] = (T)v[i].y; d[2] = (T)v[i].z; d[3] = (T)v[i].w;
       }
     }
+    const T* src = src0 + (long long)b * 32 * rl;
+    for (int e = 4 * (tid + PER * nthr); e < n; e += 4 * nthr) {   // (< 128 threads)
+      const int r = e / rl, c = e - r * rl;
+      for (int j = 0; j < 4; ++j) buf[r * YS + c + j] = src[e + j];
+    }
+  };
+  auto stage_plain = [&](int b, T* buf) {                  // FP64 / unaligned rows
+    const T* src = src0 + (long long)b * 32 * rl;
+    const int n = rows_of(b) * rl;
+    for (int e = tid; e < n; e += nthr) {
+      const int r = e / rl;
+      buf[r * YS + (e - r * rl)] = src[e];
+    }
+  };
+  if (nblk > 0) {
+    if (vec) {
+      load_regs(0);
+      store_regs(0, ys[0]);
+    } else {
+      stage_plain(0, ys[0]);
+    }
   }
-  __syncthreads();
-  if (u >= K) return;
-  T y[2 * MT];
+  // theta of user u once (shared, broadcast reads): conj(Theta_u) . y with
+  // Theta = theta[:M] + i theta[M:]
+  const bool uvalid = u < K;
   {
-    const T* yp = ys + lane * YS;
-#pragma unroll
-    for (int k = 0; k < MT; ++k) {
-      const bool in = tvalid && k < M;
-      y[2 * k] = in ? yp[2 * k] : T(0);
-      y[2 * k + 1] = in ? yp[2 * k + 1] : T(0);
+    const T* th = theta + ((long long)f * K + (uvalid ? u : 0)) * 2 * M;
+    for (int k = lane; k < MT; k += 32) {
+      tvs[threadIdx.y][k] = (uvalid && k < M) ? th[k] : T(0);
+      tvs[threadIdx.y][MT + k] = (uvalid && k < M) ? th[M + k] : T(0);
     }
   }
-  // linear part: conj(Theta_u) . y  (Theta = theta[:M] + i theta[M:])
-  const T* th = theta + ((long long)f * K + u) * 2 * M;
-  T lr = T(0), li = T(0);
-  if (M == MT) {                                   // the common case: static indices,
-    T tv[2 * MT];                                  // theta in 16-byte loads
-    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-      for (int q = 0; q < MT / 2; ++q) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(th) + q);
-        tv[4 * q] = a.x; tv[4 * q + 1] = a.y; tv[4 * q + 2] = a.z; tv[4 * q + 3] = a.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < MT; ++q) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(th) + q);
-        tv[2 * q] = a.x; tv[2 * q + 1] = a.y;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < MT; ++k) {
-      const T tr = tv[k], ti = tv[MT + k];
-      lr = fma(tr, y[2 * k], fma(ti, y[2 * k + 1], lr));
-      li = fma(tr, y[2 * k + 1], fma(-ti, y[2 * k], li));
-    }
-  } else {
-    for (int k = 0; k < M; ++k) {
-      const T tr = th[k], ti = th[M + k];
-      lr = fma(tr, ys[lane * YS + 2 * k], fma(ti, ys[lane * YS + 2 * k + 1], lr));
-      li = fma(tr, ys[lane * YS + 2 * k + 1], fma(-ti, ys[lane * YS + 2 * k], li));
-    }
-  }
-  T gr = T(0), gi = T(0);
-  const T* cu = coeff + ((long long)f * K + u) * Np;
+  const T* tv = tvs[threadIdx.y];
+  const T* cu = coeff + ((long long)f * K + (uvalid ? u : 0)) * Np;
   const char* ws = reinterpret_cast<const char*>(live);
   const int* cntp = reinterpret_cast<const int*>(ws + ws_live(gridDim.z, n_train, n_data));
   const float4* vals = reinterpret_cast<const float4*>(
       ws + (ws_live(gridDim.z, n_train, n_data) + ws_cnt(gridDim.z, n_data) + 15) / 16 * 16);
-  const int nl = tvalid ? cntp[(long long)f * n_data + t] : 0;
-  if (tvalid && w_g != T(0) && nl >= 0) {               // the screen's compact list
-    const float4* vt = vals + ((long long)f * n_data + t) * SC_CAP;
-    for (int j = 0; j < nl; ++j) {
-      const float4 v = vt[j];
-      const int p = __float_as_int(v.w);
-      const T c1 = cu[2 * p], c2 = cu[2 * p + 1];
-      const T ka = (T)v.x, kb = (T)v.y, kc = (T)v.z;
-      gr = fma(c1, ka, fma(c2, kc, gr));
-      gi = fma(c1, kb, fma(c2, ka, gi));
+  unsigned long long be = 0, se = 0;
+  for (int b = 0; b < nblk; ++b) {
+    if constexpr (NBUF == 1) {
+      if (b > 0) {
+        __syncthreads();                                    // block b - 1 finished
+        stage_plain(b, ys[0]);
+      }
     }
-  } else if (tvalid && w_g != T(0)) {                   // too many live pilots: recompute
-    const unsigned* lf = live + (long long)f * NW * n_data + t;
-    for (int w0 = 0; w0 < NW; w0 += 8) {
-      unsigned wb[8];
+    __syncthreads();                                        // rows of block b staged
+    const bool more = b + 1 < nblk;
+    if constexpr (NBUF == 2) {
+      if (more) {
+        if (vec) load_regs(b + 1);                          // in flight during block b
+        else stage_plain(b + 1, ys[(b + 1) & 1]);
+      }
+    }
+    const T* yb = ys[NBUF == 2 ? (b & 1) : 0];
+    const int t = (blk0 + b) * 32 + lane;
+    const bool tvalid = t < n_data && uvalid;
+    const int nl = tvalid ? cntp[(long long)f * n_data + t] : 0;
+    const unsigned txl = (tvalid && tx_labels) ? tx_labels[((long long)f * K + u) * n_data + t] : 0u;
+    // the symbol's row straight from shared memory (no register copy: the
+    // CTA keeps its occupancy); theta entries past M are zero
+    const T* yp = yb + lane * YS;
+    T lr = T(0), li = T(0);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) wb[q] = (w0 + q < NW) ? lf[(long long)(w0 + q) * n_data] : 0u;
+    for (int k = 0; k < MT; ++k) {
+      const T tr = tv[k], ti = tv[MT + k];
+      const T yr = k < M ? yp[2 * k] : T(0), yi = k < M ? yp[2 * k + 1] : T(0);
+      lr = fma(tr, yr, fma(ti, yi, lr));
+      li = fma(tr, yi, fma(-ti, yr, li));
+    }
+    T gr = T(0), gi = T(0);
+    if (tvalid && w_g != T(0) && nl >= 0) {                 // the screen's compact list
+      const float4* vt = vals + ((long long)f * n_data + t) * SC_CAP;
+      for (int j = 0; j < nl; ++j) {
+        const float4 vv = vt[j];
+        const int p = __float_as_int(vv.w);
+        const T c1 = cu[2 * p], c2 = cu[2 * p + 1];
+        const T ka = (T)vv.x, kb = (T)vv.y, kc = (T)vv.z;
+        gr = fma(c1, ka, fma(c2, kc, gr));
+        gi = fma(c1, kb, fma(c2, ka, gi));
+      }
+    } else if (tvalid && w_g != T(0)) {                     // too many live pilots: recompute
+      const unsigned* lf = live + (long long)f * NW * n_data + t;
+      for (int w0 = 0; w0 < NW; w0 += 8) {
+        unsigned wb[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        unsigned b = wb[q];
-        while (b) {
-          const int p = (w0 + q) * 32 + __ffs(b) - 1;
-          b &= b - 1;
-          const T* x = Xf + (long long)p * 2 * M;
-          const T c1 = cu[2 * p], c2 = cu[2 * p + 1];
-          T ea = T(0), eb = T(0), ec = T(0);
+        for (int q = 0; q < 8; ++q) wb[q] = (w0 + q < NW) ? lf[(long long)(w0 + q) * n_data] : 0u;
 #pragma unroll
-          for (int k = 0; k < MT; ++k) {
-            if (k < M) {
-              const T xr = x[2 * k], xi = x[2 * k + 1], yr = y[2 * k], yi = y[2 * k + 1];
-              T a0 = xr - yr, a1 = xi - yi;
-              ea = fma(a0, a0, fma(a1, a1, ea));
-              a0 = xr - yi; a1 = xi + yr;
-              eb = fma(a0, a0, fma(a1, a1, eb));
-              a0 = xr + yi; a1 = xi - yr;
-              ec = fma(a0, a0, fma(a1, a1, ec));
+        for (int q = 0; q < 8; ++q) {
+          unsigned bb = wb[q];
+          while (bb) {
+            const int p = (w0 + q) * 32 + __ffs(bb) - 1;
+            bb &= bb - 1;
+            const T* x = Xf + (long long)p * 2 * M;
+            const T c1 = cu[2 * p], c2 = cu[2 * p + 1];
+            T ea = T(0), eb = T(0), ec = T(0);
+#pragma unroll
+            for (int k = 0; k < MT; ++k) {
+              if (k < M) {
+                const T xr = x[2 * k], xi = x[2 * k + 1], yr = yp[2 * k], yi = yp[2 * k + 1];
+                T a0 = xr - yr, a1 = xi - yi;
+                ea = fma(a0, a0, fma(a1, a1, ea));
+                a0 = xr - yi; a1 = xi + yr;
+                eb = fma(a0, a0, fma(a1, a1, eb));
+                a0 = xr + yi; a1 = xi - yr;
+                ec = fma(a0, a0, fma(a1, a1, ec));
+              }
             }
+            const T ka = exp_fast(-ea * inv2s), kb = exp_fast(-eb * inv2s), kc = exp_fast(-ec * inv2s);
+            gr = fma(c1, ka, fma(c2, kc, gr));
+            gi = fma(c1, kb, fma(c2, ka, gi));
           }
-          const T ka = exp_fast(-ea * inv2s), kb = exp_fast(-eb * inv2s), kc = exp_fast(-ec * inv2s);
-          gr = fma(c1, ka, fma(c2, kc, gr));
-          gi = fma(c1, kb, fma(c2, ka, gi));
         }
       }
     }
-  }
-  const T er = lr + w_g * gr, ei = li + w_g * gi;
-  int best = 0;
-  T bd = T(0);
-  for (int q = 0; q < n_points; ++q) {
-    const T dr = er - pts[2 * q], di = ei - pts[2 * q + 1];
-    const T d = dr * dr + di * di;
-    if (q == 0 || d < bd) { bd = d; best = q; }
-  }
-  unsigned long long be = 0, se = 0;
-  if (tvalid) {
-    const long long o = ((long long)f * K + u) * n_data + t;
-    if (est_out) { est_out[2 * o] = er; est_out[2 * o + 1] = ei; }
-    if (labels_out) labels_out[o] = (unsigned char)best;
-    if (tx_labels) {
-      const unsigned tx = tx_labels[o];
-      be = __popc((unsigned)best ^ tx);
-      se = ((unsigned)best != tx) ? 1ull : 0ull;
+    const T er = lr + w_g * gr, ei = li + w_g * gi;
+    int best = 0;
+    T bd = T(0);
+    for (int q = 0; q < n_points; ++q) {
+      const T dr = er - pts[2 * q], di = ei - pts[2 * q + 1];
+      const T d = dr * dr + di * di;
+      if (q == 0 || d < bd) { bd = d; best = q; }
+    }
+    if (tvalid) {
+      const long long o = ((long long)f * K + u) * n_data + t;
+      if (est_out) { est_out[2 * o] = er; est_out[2 * o + 1] = ei; }
+      if (labels_out) labels_out[o] = (unsigned char)best;
+      if (tx_labels) {
+        be += __popc((unsigned)best ^ txl);
+        se += ((unsigned)best != txl) ? 1ull : 0ull;
+      }
+    }
+    if constexpr (NBUF == 2) {
+      if (more && vec) store_regs(b + 1, ys[(b + 1) & 1]); // (read after the next barrier)
     }
   }
-  if (tx_labels && (bit_err || sym_err)) {
+  if (uvalid && tx_labels && (bit_err || sym_err)) {
     const unsigned long long bsum = warp_sum_u64(be), ssum = warp_sum_u64(se);
     if (lane == 0) {
       if (bit_err && bsum) atomicAdd(&bit_err[(long long)f * K + u], bsum);
@@ -439,11 +458,15 @@ int launch_finish(const T* rx, long long rx_stride, int F, int K, int n_train, i
   // payload rows staged once; 4 for a few frames, where more, smaller CTAs
   // shorten the single-frame latency
   const int ku = (MT <= 16 && sizeof(T) == 4 && F >= 8) ? (K < 8 ? K : 8) : 4;
+  // symbol blocks per CTA: 4 for batches (one latency per 128 symbols), 1 for
+  // a few frames (more CTAs: a shorter single-frame critical path)
+  const int nb = F >= 8 ? 4 : 1;
+  const int nblocks = (n_data + 31) / 32;
   dim3 block(32, ku);
-  dim3 grid((n_data + 31) / 32, (K + ku - 1) / ku, F);
+  dim3 grid((nblocks + nb - 1) / nb, (K + ku - 1) / ku, F);
   detect_finish_kernel<T, MT><<<grid, block, 0, s>>>(
       rx, rx_stride, K, n_train, n_data, M, coeff, theta, (T)p.w_g,
-      (T)(1.0 / (2.0 * p.sigma_sq)), points, n_points, tx, live, est, labels, be, se);
+      (T)(1.0 / (2.0 * p.sigma_sq)), points, n_points, tx, live, est, labels, be, se, nb);
   return status_from(cudaGetLastError());
 }
 

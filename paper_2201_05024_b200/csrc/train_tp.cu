@@ -402,7 +402,8 @@ __global__ void __launch_bounds__(128, 6)
     cp_async_commit();
     if (!MAIN && n < 0) return;
     // ---- step n: the window's deltas, then the window update ----
-    const int lo = n - W + 1 > 0 ? n - W + 1 : 0, cj = n - lo;
+    const int lo = MAIN ? n - W + 1 : (n - W + 1 > 0 ? n - W + 1 : 0);
+    const int cj = MAIN ? W - 1 : n - lo;
     float qm = qmc, ql = qlc;
     if (!MAIN) {
       qm = qs[2 * cj];
