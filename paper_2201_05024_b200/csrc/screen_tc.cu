@@ -169,7 +169,14 @@ __global__ void __launch_bounds__(TC_THREADS)
   const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
   const float* Xf = rx + (long long)f * rx_stride;
   const float* Yf = Xf + (long long)y_row0 * D;           // the "payload" rows
-  const int n_mt = (n_train + TC_MROWS - 1) / TC_MROWS;
+  // pilot tiles this CTA needs: all of them for the detection; for the
+  // trainer's pilot screen (list_max_off < 0) only those holding pilots
+  // p <= t + list_max_off of its rows (the lower triangle); the live words of
+  // the skipped tiles are written as zeros
+  const int n_mt_all = (n_train + TC_MROWS - 1) / TC_MROWS;
+  const int n_mt = list_max_off < 0
+                       ? max(0, min(n_mt_all, (t0 + NT - 1 + list_max_off) / TC_MROWS + 1))
+                       : n_mt_all;
 
   if (tid == 0) {
     mbar_init(mbar, 1);
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS)
     }
     cp_async_commit();
   };
-  load_a(0, 0);
+  if (n_mt > 0) load_a(0, 0);
 
   fence_async_smem();
   tc_fence_before();
@@ -408,6 +415,11 @@ __global__ void __launch_bounds__(TC_THREADS)
     }
     tc_fence_before();
   }
+  }
+  // live words of the skipped pilot tiles (pilot screen's upper triangle)
+  for (int i = tid; i < (NW - n_mt * (TC_MROWS / 32)) * NT; i += TC_THREADS) {
+    const int w = n_mt * (TC_MROWS / 32) + i / NT, sy = i % NT;
+    if (!GB || t0 + sy < n_data) bits[w * BST + sy] = 0u;
   }
   __syncthreads();
   if (warp == 0)
