@@ -56,7 +56,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--batch", type=int, default=1024, help="frames per step per GPU")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="frames per step per GPU (default 8 per SM: 1184 on a B200 -- "
+                         "6 chains per frame, the trainer's two full waves of 24 chains per SM)")
     ap.add_argument("--lat-samples", type=int, default=1000)
     ap.add_argument("--inflight", type=int, default=6,
                     help="single-frame streaming: frames in flight (FrameStream depth)")
@@ -312,7 +314,7 @@ def main():
         return 2
     dev = torch.device("cuda", torch.cuda.current_device())
     lib = _lib.load()
-    B = args.batch
+    B = args.batch or 8 * torch.cuda.get_device_properties(dev).multi_processor_count
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def barrier():
