@@ -556,7 +556,9 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(f"{dom}_batch{B}_bytes_per_launch")
+            tr = json.load(open(tr_path))
+            if tr.get("batch_frames") == B:     # the capture of this batch size
+                traffic = tr.get(f"{dom}_batch_bytes_per_launch")
         except Exception:
             traffic = None
     # the single-frame trainer is a chain of 2 n_train dependent steps per user:
