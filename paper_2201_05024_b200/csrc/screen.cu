@@ -460,7 +460,7 @@ int launch_finish(const T* rx, long long rx_stride, int F, int K, int n_train, i
   const int ku = (MT <= 16 && sizeof(T) == 4 && F >= 8) ? (K < 8 ? K : 8) : 4;
   // symbol blocks per CTA: 4 for batches (one latency per 128 symbols), 1 for
   // a few frames (more CTAs: a shorter single-frame critical path)
-  const int nb = F >= 8 ? 8 : 1;
+  const int nb = (F >= 8 && sizeof(T) == 4) ? 8 : 1;       // (FP64: one staging buffer)
   const int nblocks = (n_data + 31) / 32;
   dim3 block(32, ku);
   dim3 grid((nblocks + nb - 1) / nb, (K + ku - 1) / ku, F);
