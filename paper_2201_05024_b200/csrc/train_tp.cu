@@ -187,7 +187,7 @@ KAPSM_DEV float rcomp(const float* x, int e, int beta) {
   return (e & 1) ? -x[e - 1] : x[e + 1];
 }
 
-template <int DPL>
+template <int DPL, bool VEC>
 __global__ void __launch_bounds__(128, 6)
     apsm_train_tp_kernel(const float* __restrict__ rx, long long rx_stride,
                          const float* __restrict__ targets, const float* __restrict__ kband,
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(128, 6)
   const float4* LV = pvals + (long long)f * n_train * TP_CAP;
   float* Cout = coeff_out + (long long)task * Np;
   int* FSout = fs_out + (long long)task * Np;
-  const bool vec = (D % 4) == 0 && (rx_stride % 4) == 0 && ((size_t)rx & 15) == 0;
+  constexpr bool vec = VEC;       // 16-byte rows (host: D % 4 == 0, aligned rows)
   const bool gauss = w_g != 0.f;
 
   for (int i = lane; i < TP_RING * TP_KS; i += 32) Ks[i] = 0.f;
@@ -241,12 +241,15 @@ __global__ void __launch_bounds__(128, 6)
   // advanced by gm + (mm odd) gt per step.
   const int XP = vec ? D / 4 : D, NPC = 2 * XP + 10;
   const unsigned sg_s = sbase + L::STG;
-  const char* pp[3];
-  long long pgm[3], pgt[3];
-  unsigned ps[3];
-  int psz[3], poff[3];           // poff: the piece's sample is m - poff
+  // pieces per lane (compile time): 2 rows of up to 8 DPL 16-byte pieces (or
+  // 32 DPL 4-byte ones) + 8 band pieces + target + live count
+  constexpr int NRP = VEC ? (16 * DPL + 10 + 31) / 32 : (64 * DPL + 10 + 31) / 32;
+  const char* pp[NRP];
+  long long pgm[NRP], pgt[NRP];
+  unsigned ps[NRP];
+  int psz[NRP], poff[NRP];       // poff: the piece's sample is m - poff
 #pragma unroll
-  for (int r = 0; r < 3; ++r) {
+  for (int r = 0; r < NRP; ++r) {
     int pc = lane + 32 * r;
     const char* g = nullptr;
     pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; poff[r] = 0;
@@ -279,19 +282,17 @@ __global__ void __launch_bounds__(128, 6)
     const long long mm0 = -poff[r];
     pp[r] = g ? g + mm0 * pgm[r] + (mm0 >> 1) * pgt[r] : nullptr;
   }
-  const int nr = (NPC + 31) / 32;
+  (void)NPC;
   int pm = 0;                    // the sample index m of the next prefetch
   auto prefetch = [&]() {        // stage of sample pm (steps are prefetched in order)
     const unsigned so = (unsigned)((pm & (TP_STG - 1)) * SSTR) * 4;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      if (r < nr) {
-        const int mm = pm - poff[r];
-        const bool go = (unsigned)mm < (unsigned)Np;
-        cpa16_if(go && psz[r] == 16, ps[r] + so, pp[r]);
-        cpa4_if(go && psz[r] == 4, ps[r] + so, pp[r]);
-        pp[r] += pgm[r] + ((mm & 1) ? pgt[r] : 0);          // -> sample mm + 1
-      }
+    for (int r = 0; r < NRP; ++r) {
+      const int mm = pm - poff[r];
+      const bool go = (unsigned)mm < (unsigned)Np;
+      cpa16_if(go && psz[r] == 16, ps[r] + so, pp[r]);
+      cpa4_if(go && psz[r] == 4, ps[r] + so, pp[r]);
+      pp[r] += pgm[r] + ((mm & 1) ? pgt[r] : 0);            // -> sample mm + 1
     }
     ++pm;
   };
@@ -591,17 +592,19 @@ __global__ void __launch_bounds__(32 * NW, 1)
   }
   if (tid == 0) red[0] = red[1] = 0;
 
-  // prefetch pieces of step m's stage, spread over the CTA (<= 2 per thread):
+  // prefetch pieces of step m's stage, spread over the CTA:
   // pilot rows of m and of the leaving sample m - SPAN + 1, the band row (R/4
   // pieces), the live-list row (8), the target, the live count
   const int XP = vec ? D / 4 : D, NPC = 2 * XP + R / 4 + 10;
   const unsigned sg_s = smem_u32(smem_tp) + L::STG;
-  const char* pp[2];
-  long long pgm[2], pgt[2];
-  unsigned ps[2];
-  int psz[2], poff[2];
+  // rounds of pieces per thread: enough for 4-byte pieces of the widest row
+  constexpr int PRW = (2 * 32 * DPL + R / 4 + 10 + NT - 1) / NT;
+  const char* pp[PRW];
+  long long pgm[PRW], pgt[PRW];
+  unsigned ps[PRW];
+  int psz[PRW], poff[PRW];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < PRW; ++r) {
     int pc = tid + NT * r;
     const char* g = nullptr;
     pgm[r] = 0; pgt[r] = 0; ps[r] = sg_s; psz[r] = 0; poff[r] = 0;
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   auto prefetch = [&]() {
     const unsigned so = (unsigned)((pm & (TPW_STG - 1)) * SSTR) * 4;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < PRW; ++r) {
       if (r < nr) {
         const int mm = pm - poff[r];
         const bool go = (unsigned)mm < (unsigned)Np;
@@ -1435,9 +1438,15 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
     int wpc = lat ? 1 : 4;
     while (wpc > 1 && (size_t)tp_total(M) * wpc > 227 * 1024) wpc >>= 1;
     const size_t smem = (size_t)tp_total(M) * wpc;
-    if (DPL == 1) return launch(apsm_train_tp_kernel<1>, wpc, 32 * wpc, smem);
-    if (DPL == 2) return launch(apsm_train_tp_kernel<2>, wpc, 32 * wpc, smem);
-    return launch(apsm_train_tp_kernel<4>, wpc, 32 * wpc, smem);
+    const bool vec = (2 * M) % 4 == 0 && rx_stride % 4 == 0 && ((size_t)rx & 15) == 0;
+    if (vec) {
+      if (DPL == 1) return launch(apsm_train_tp_kernel<1, true>, wpc, 32 * wpc, smem);
+      if (DPL == 2) return launch(apsm_train_tp_kernel<2, true>, wpc, 32 * wpc, smem);
+      return launch(apsm_train_tp_kernel<4, true>, wpc, 32 * wpc, smem);
+    }
+    if (DPL == 1) return launch(apsm_train_tp_kernel<1, false>, wpc, 32 * wpc, smem);
+    if (DPL == 2) return launch(apsm_train_tp_kernel<2, false>, wpc, 32 * wpc, smem);
+    return launch(apsm_train_tp_kernel<4, false>, wpc, 32 * wpc, smem);
   }
   // wide windows: one CTA of R / 32 warps per chain
   const int NW = R / 32;

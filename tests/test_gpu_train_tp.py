@@ -124,3 +124,27 @@ def test_wide_ring_trainer_matches_oracle(W, M, Kn, nt, scheme):
         assert maxrel(r["theta"][0, u], ref["theta"]) < 1e-4
         est = O.detect_batch(ref["theta"], ref["atoms"], ref["coeffs"], rx[0, nt:])
         assert maxrel(r["est"][0, u], est) < 1e-4
+
+
+@pytest.mark.parametrize("W", [20, 40])
+def test_band_trainers_odd_antenna_count(W):
+    """Odd M (rows not a multiple of 16 bytes: the 4-byte prefetch pieces),
+    M = 19 (two 32-float row chunks), more chains than SMs (one-warp form at
+    W = 20, one CTA per chain at W = 40) and a single frame (ring warps +
+    helpers): atoms, slot order, coefficients and theta vs the oracle."""
+    Kn, M, nt, nd = 6, 19, 90, 60
+    for F in (30, 1):
+        seeds = list(range(300, 300 + F))
+        rx, pil, tx, _ = K.host_frames(seeds, Kn, M, nt, nd, "QPSK")
+        pipe = K.FramePipeline(F, Kn, M, nt, nd, "QPSK", cfg=K.ApsmConfig(window=W),
+                               precision="f32")
+        pipe.load(rx, pil, tx)
+        pipe.launch_trainer(2)
+        r = pipe.results()
+        for f in sorted({0, F - 1}):
+            for u, ref in enumerate(_oracle_users(rx[f], pil[f], nt, W, (0, Kn - 1))):
+                uu = (0, Kn - 1)[u]
+                assert int(r["n_active"][f, uu]) == ref["n_atoms"], (F, f, uu)
+                assert np.array_equal(r["first_step"][f, uu], ref["first_step"])
+                assert maxrel(r["coeff"][f, uu], ref["coeff"]) < 1e-4
+                assert maxrel(r["theta"][f, uu], ref["theta"]) < 1e-4
