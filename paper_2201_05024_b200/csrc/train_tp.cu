@@ -17,7 +17,7 @@
 //   * K[j][m] (sum kernel, w_l r.r + w_g kappa_G, explicit differences) for
 //     all ring pairs is a 32 x 32 shared matrix; a takeover writes the new
 //     sample's row and column from the band K[m][m-d], d < 32, made by
-//     band_kernel below (no pilot Gram matrix is materialised);
+//     band_tile_kernel below (no pilot Gram matrix is materialised);
 //   * at takeover, f_{m-P}(r_m) = w_l theta_fin . r_m + sum_{j in window} c_j K[j][m]
 //       + w_g sum_{a <= m-P-W live} c_a kappa_G(r_a, r_m),
 //     theta_fin = sum of c_a r_a over the samples that already left the window
@@ -106,62 +106,90 @@ KAPSM_DEV void stg_if<int>(bool p, int* dst, int v) {
 // distances |x - y|, |x + iy|, |x - iy| by explicit differences, hence the
 // 2 x 2 realified block: linear parts Re c, Im c, -Im c, Re c and Gaussian
 // parts of the matching distances (as screen.cu's list values).
+// Tiled: a CTA stages TT pilot rows of a frame plus the R/2 rows before them
+// in shared memory with contiguous 16-byte loads (padded rows: the 16-byte
+// reads of 8 different rows hit different banks), forms every pair (t, t - dt)
+// of the tile from shared memory (one thread per pair), collects the tile's
+// 2 TT band rows in shared memory and writes them out as one contiguous block.  Global traffic is the compulsory rows and
+// band, with many requests in flight per CTA (a thread-per-pair kernel reading
+// rows from global memory waited a DRAM round trip per thread: 2x slower).
 __global__ void __launch_bounds__(256)
-    band_kernel(const float* __restrict__ rx, long long rx_stride, int n_train, int M, float w_l,
-                float w_g, float inv2s, float* __restrict__ kband, int R) {
-  const int Np = 2 * n_train, D = 2 * M, H = R / 2 + 1;
-  const int f = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_train * H) return;
-  const int t = i / H, dt = i - t * H, tp = t - dt;
-  float* kb = kband + (long long)f * Np * R;
-  if (tp < 0) {                                           // before the first sample: zeros
+    band_tile_kernel(const float* __restrict__ rx, long long rx_stride, int n_train, int M,
+                     float w_l, float w_g, float inv2s, float* __restrict__ kband, int R, int TT) {
+  extern __shared__ __align__(16) float bsm[];
+  const int Np = 2 * n_train, D = 2 * M, H = R / 2;
+  const int DS = ((D + 3) & ~3) + 4;                      // padded row stride (floats)
+  const int f = blockIdx.y, t0 = blockIdx.x * TT;
+  const int r0 = max(0, t0 - H), r1 = min(n_train, t0 + TT);   // staged rows [r0, r1)
+  float* rows = bsm;                                      // [(TT + H)][DS]
+  float* out = bsm + (size_t)(TT + H) * DS;               // [2 TT][R]
+  const float* X = rx + (long long)f * rx_stride;
+  const bool v16 = (D & 3) == 0 && (rx_stride & 3) == 0 && ((size_t)rx & 15) == 0;
+  if (v16) {
+    const int q4 = D / 4, n4 = (r1 - r0) * q4;
+    const float4* src = reinterpret_cast<const float4*>(X + (long long)r0 * D);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+      const int r = i / q4, c = i - r * q4;
+      *reinterpret_cast<float4*>(rows + r * DS + 4 * c) = __ldg(src + i);
+    }
+  } else {
+    const int n = (r1 - r0) * D;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int r = i / D;
+      rows[r * DS + (i - r * D)] = X[(long long)r0 * D + i];
+    }
+  }
+  __syncthreads();
+  const int pairs = TT * (H + 1);
+  const bool gauss = w_g != 0.f;
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int tt = i / (H + 1), dt = i - tt * (H + 1), t = t0 + tt, tp = t - dt;
+    if (t >= n_train) continue;
+    float vals[2][2] = {{0.f, 0.f}, {0.f, 0.f}};          // [alpha][beta]
+    if (tp >= 0) {
+      const float* y = rows + (t - r0) * DS;
+      const float* x = rows + (tp - r0) * DS;
+      float cr = 0.f, ci = 0.f, ea = 0.f, eb = 0.f, ec = 0.f;
+      auto acc = [&](float xr, float xi, float yr, float yi) {
+        cr = fmaf(xr, yr, fmaf(xi, yi, cr));
+        ci = fmaf(xr, yi, fmaf(-xi, yr, ci));
+        float a0 = xr - yr, a1 = xi - yi;
+        ea = fmaf(a0, a0, fmaf(a1, a1, ea));
+        a0 = xr - yi; a1 = xi + yr;
+        eb = fmaf(a0, a0, fmaf(a1, a1, eb));
+        a0 = xr + yi; a1 = xi - yr;
+        ec = fmaf(a0, a0, fmaf(a1, a1, ec));
+      };
+      if ((D & 3) == 0) {
+        for (int q = 0; q < D / 4; ++q) {
+          const float4 xv = *reinterpret_cast<const float4*>(x + 4 * q);
+          const float4 yv = *reinterpret_cast<const float4*>(y + 4 * q);
+          acc(xv.x, xv.y, yv.x, yv.y);
+          acc(xv.z, xv.w, yv.z, yv.w);
+        }
+      } else {
+        for (int k = 0; k < M; ++k) acc(x[2 * k], x[2 * k + 1], y[2 * k], y[2 * k + 1]);
+      }
+      const float ka = gauss ? (dt == 0 ? 1.f : exp_fast(-ea * inv2s)) : 0.f;
+      const float kbv = gauss ? exp_fast(-eb * inv2s) : 0.f;
+      const float kc = gauss ? exp_fast(-ec * inv2s) : 0.f;
+      vals[0][0] = vals[1][1] = w_l * cr + w_g * ka;
+      vals[0][1] = w_l * ci + w_g * kbv;                  // r1(x) . r2(y) = Im(x^H y)
+      vals[1][0] = -w_l * ci + w_g * kc;                  // r2(x) . r1(y) = -Im(x^H y)
+    }
     for (int be = 0; be < 2; ++be)
       for (int al = 0; al < 2; ++al) {
         const int d = 2 * dt + be - al;
-        if (d >= 0 && d < R) kb[(long long)(2 * t + be) * R + d] = 0.f;
+        if (d >= 0 && d < R) out[(2 * tt + be) * R + d] = vals[al][be];
       }
-    return;
   }
-  const float* X = rx + (long long)f * rx_stride;
-  const float* y = X + (long long)t * D;
-  const float* x = X + (long long)tp * D;
-  float cr = 0.f, ci = 0.f, ea = 0.f, eb = 0.f, ec = 0.f;
-  auto acc = [&](float xr, float xi, float yr, float yi) {
-    cr = fmaf(xr, yr, fmaf(xi, yi, cr));
-    ci = fmaf(xr, yi, fmaf(-xi, yr, ci));
-    float a0 = xr - yr, a1 = xi - yi;
-    ea = fmaf(a0, a0, fmaf(a1, a1, ea));
-    a0 = xr - yi; a1 = xi + yr;
-    eb = fmaf(a0, a0, fmaf(a1, a1, eb));
-    a0 = xr + yi; a1 = xi - yr;
-    ec = fmaf(a0, a0, fmaf(a1, a1, ec));
-  };
-  if ((D & 3) == 0 && (rx_stride & 3) == 0 && ((size_t)rx & 15) == 0) {
-#pragma unroll 8
-    for (int q = 0; q < D / 4; ++q) {            // 16-byte loads: two antennas each
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + q);
-      const float4 yv = __ldg(reinterpret_cast<const float4*>(y) + q);
-      acc(xv.x, xv.y, yv.x, yv.y);
-      acc(xv.z, xv.w, yv.z, yv.w);
-    }
-  } else {
-    for (int k = 0; k < M; ++k) acc(x[2 * k], x[2 * k + 1], y[2 * k], y[2 * k + 1]);
-  }
-  const bool gauss = w_g != 0.f;
-  const float ka = gauss ? (dt == 0 ? 1.f : exp_fast(-ea * inv2s)) : 0.f;
-  const float kbv = gauss ? exp_fast(-eb * inv2s) : 0.f;
-  const float kc = gauss ? exp_fast(-ec * inv2s) : 0.f;
-  // (alpha, beta) of a = 2(t - dt) + alpha, m = 2t + beta
-  const float v00 = w_l * cr + w_g * ka, v11 = v00;
-  const float v01 = w_l * ci + w_g * kbv;                 // r1(x) . r2(y) = Im(x^H y)
-  const float v10 = -w_l * ci + w_g * kc;                 // r2(x) . r1(y) = -Im(x^H y)
-  const float vals[2][2] = {{v00, v01}, {v10, v11}};      // [alpha][beta]
-  for (int be = 0; be < 2; ++be)
-    for (int al = 0; al < 2; ++al) {
-      const int d = 2 * dt + be - al;
-      if (d >= 0 && d < R) kb[(long long)(2 * t + be) * R + d] = vals[al][be];
-    }
+  __syncthreads();
+  // the tile's band rows 2 t0 .. 2 min(t0 + TT, n_train) - 1: one contiguous block
+  const int nrow = 2 * (min(t0 + TT, n_train) - t0);
+  float* kb = kband + (long long)f * Np * R + (long long)2 * t0 * R;
+  const int n4 = nrow * R / 4;                            // R is a multiple of 32
+  for (int i = threadIdx.x; i < n4; i += blockDim.x)
+    reinterpret_cast<float4*>(kb)[i] = reinterpret_cast<const float4*>(out)[i];
 }
 
 KAPSM_DEV float warp_sum_f(float v) {
@@ -1379,9 +1407,17 @@ int train_tp(const float* rx, long long rx_stride, const float* targets, int F, 
   float4* pvals = reinterpret_cast<float4*>(w);
   const float inv2s = (float)(1.0 / (2.0 * p.sigma_sq));
   if (stages & 1) {
-    dim3 grid((unsigned)(((long long)n_train * (R / 2 + 1) + 255) / 256), F);
-    band_kernel<<<grid, 256, 0, s>>>(rx, rx_stride, n_train, M, (float)p.w_l, (float)p.w_g, inv2s,
-                                     kband, R);
+    // tiles of TT pilots: shared rows (TT + R/2) x (2M + 4) floats + band 2 TT x R
+    const int DS = ((2 * M + 3) & ~3) + 4;
+    int TT = 128;
+    while (TT > 16 && ((size_t)(TT + R / 2) * DS + (size_t)2 * TT * R) * 4 > 100 * 1024) TT >>= 1;
+    const size_t smem = ((size_t)(TT + R / 2) * DS + (size_t)2 * TT * R) * 4;
+    if (cudaFuncSetAttribute(band_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return KAPSM_ERR_CUDA;
+    dim3 grid((unsigned)((n_train + TT - 1) / TT), F);
+    band_tile_kernel<<<grid, 256, smem, s>>>(rx, rx_stride, n_train, M, (float)p.w_l,
+                                             (float)p.w_g, inv2s, kband, R, TT);
     if (cudaGetLastError() != cudaSuccess) return KAPSM_ERR_CUDA;
   }
   const int tasks = F * K;
