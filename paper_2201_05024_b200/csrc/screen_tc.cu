@@ -190,15 +190,28 @@ __global__ void __launch_bounds__(TC_THREADS)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
-  // ---- B: NT payload rows (Re) and their rotations (Im), zero past n_data ----
-  for (int e = tid; e < NT * KC * 8; e += TC_THREADS) {
-    const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
-    const int t = t0 + r;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < n_data) v = row_f4(Yf + (long long)t * D, kc * 8 + j, D, vec);
-    const unsigned chunk = (unsigned)kc * (2 * NT) * 128;
-    sts_f4(sB + chunk + sw128_off(r, j), v);
-    sts_f4(sB + chunk + sw128_off(NT + r, j), make_float4(v.y, -v.x, v.w, -v.z));
+  // ---- B: NT payload rows (Re) and their rotations (Im), zero past n_data;
+  //      a thread's loads are all issued before its stores (one memory
+  //      latency per CTA instead of one per piece) ----
+  {
+    constexpr int PER = NT * KC * 8 / TC_THREADS;
+    float4 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * TC_THREADS;
+      const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
+      const int t = t0 + r;
+      v[i] = t < n_data ? row_f4(Yf + (long long)t * D, kc * 8 + j, D, vec)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * TC_THREADS;
+      const int r = e / (KC * 8), rem = e - r * (KC * 8), kc = rem >> 3, j = rem & 7;
+      const unsigned chunk = (unsigned)kc * (2 * NT) * 128;
+      sts_f4(sB + chunk + sw128_off(r, j), v[i]);
+      sts_f4(sB + chunk + sw128_off(NT + r, j), make_float4(v[i].y, -v[i].x, v[i].w, -v[i].z));
+    }
   }
 
   // ---- A tile loader: pilots p0 .. p0 + 127 into buffer b ----
