@@ -148,3 +148,23 @@ def test_band_trainers_odd_antenna_count(W):
                 assert np.array_equal(r["first_step"][f, uu], ref["first_step"])
                 assert maxrel(r["coeff"][f, uu], ref["coeff"]) < 1e-4
                 assert maxrel(r["theta"][f, uu], ref["theta"]) < 1e-4
+
+
+@pytest.mark.parametrize("nt", [1, 2, 5, 17])
+@pytest.mark.parametrize("W,mode,F", [(20, 2, 1), (20, 3, 1), (40, 2, 1), (20, 2, 40), (40, 2, 40)])
+def test_band_trainers_tiny_pilot_blocks(nt, W, mode, F):
+    """Pilot blocks shorter than the takeover lead and the window (every step
+    range of the trainers empty or clipped): all forms against the oracle."""
+    Kn, M, nd = 6, 4, 20
+    seeds = list(range(700, 700 + F))
+    rx, pil, tx, _ = K.host_frames(seeds, Kn, M, nt, nd, "QPSK")
+    pipe = K.FramePipeline(F, Kn, M, nt, nd, "QPSK", cfg=K.ApsmConfig(window=W), precision="f32")
+    pipe.load(rx, pil, tx)
+    pipe.launch_trainer(mode)
+    r = pipe.results()
+    for f in sorted({0, F - 1}):
+        for u, ref in enumerate(_oracle_users(rx[f], pil[f], nt, W, range(Kn))):
+            assert int(r["n_active"][f, u]) == ref["n_atoms"], (nt, W, f, u)
+            assert np.array_equal(r["first_step"][f, u], ref["first_step"])
+            assert maxrel(r["coeff"][f, u], ref["coeff"]) < 1e-4
+            assert maxrel(r["theta"][f, u], ref["theta"]) < 1e-4
