@@ -50,12 +50,13 @@ __host__ __device__ constexpr int tp_lead(int W) { return TP_SPAN - W; }   // ta
 // (rows of up to 32 DPL floats); the stage of step n = m - P holds the
 // prefetched inputs of that step: the pilot row of the sample taken over (m)
 // and of the sample leaving the window (m - TP_SPAN + 1), XR floats each, then
-// the band row (32), the live-list row (8 float4), the target and the live count
+// the band row (32), the target and the live count (8 KB per chain at M <= 16;
+// 6 CTAs of 4 chains per SM, bound by the 80 registers)
 template <int DPL>
 struct TpL {
   static constexpr int XR = 32 * DPL;
-  static constexpr int SSTR = 2 * XR + 68;                  // floats per stage
-  static constexpr int OKB = 2 * XR, OLV = OKB + 32, OB = OLV + 32, OLC = OB + 1;
+  static constexpr int SSTR = 2 * XR + 36;                  // floats per stage
+  static constexpr int OKB = 2 * XR, OB = OKB + 32, OLC = OB + 1;
   static constexpr int KS = 0;                              // [32][TP_KS] K over ring pairs
   static constexpr int DSM = KS + TP_RING * TP_KS * 4;      // [32] deltas
   static constexpr int QS = DSM + TP_RING * 4;              // [32][2] (q_mid, q_last)
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(128, 6)
   const float* Sg = reinterpret_cast<const float*>(base + L::STG);  // [STG][SSTR] stages
   float* qs = reinterpret_cast<float*>(base + L::QS);      // [W][2] (q_mid, q_last)
   constexpr int XR = L::XR, SSTR = L::SSTR;
-  constexpr int OKB = L::OKB, OLV = L::OLV, OB = L::OB, OLC = L::OLC;   // stage offsets
+  constexpr int OKB = L::OKB, OB = L::OB, OLC = L::OLC;   // stage offsets
   const int f = task / K;
   const float* X = rx + (long long)f * rx_stride;
   const float* Bt = targets + (long long)task * Np;
