@@ -372,8 +372,12 @@ def main():
     rx_pin = gen.rx.view(P, *gen.rx.shape[2:])
     pil_pin = gen.pilots.view(P, *gen.pilots.shape[2:])
     tx_pin = gen.tx.view(P, *gen.tx.shape[2:])
+    plab_pin = gen.plab.view(P, *gen.plab.shape[2:])      # pilot labels (uint8)
     rx_d, pil_d, tx_d = rx_pin.to(dev), pil_pin.to(dev), tx_pin.to(dev)
+    # e2e ships the pilots as labels (1 byte per pilot and user; the receiver
+    # knows its pilot sequence), expanded into targets on the device
     frame_bytes = (rx_pin[0].numel() * 4 + pil_pin[0].numel() * 4 + tx_pin[0].numel())
+    e2e_frame_bytes = (rx_pin[0].numel() * 4 + plab_pin[0].numel() + tx_pin[0].numel())
 
     def sl(t, j, n=B):
         return t[j * n % P:j * n % P + n]
@@ -599,14 +603,14 @@ def main():
             D.gather_decisions(pp.labels)
             D.reduce_counts(torch.cat([pp.bit_err.view(-1), pp.sym_err.view(-1)]))
     fs = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32", depth=2,
-                       concurrent=True, frames=B, post=post)
-    h2d = frame_bytes * B
+                       concurrent=True, frames=B, post=post, pilot_labels=True)
+    h2d = e2e_frame_bytes * B
     d2h = (fs.labels_h[0].numel() + fs.counts_h[0].numel() * 8 + fs.status_h[0].numel() * 4)
 
     def e2e_run(n, i0, start=None):
         t = None
         for i in range(n):
-            t = fs.submit(sl(rx_pin, i0 + i), sl(pil_pin, i0 + i), sl(tx_pin, i0 + i),
+            t = fs.submit(sl(rx_pin, i0 + i), sl(plab_pin, i0 + i), sl(tx_pin, i0 + i),
                           start_event=start if i == 0 else None)
         cur = torch.cuda.current_stream()
         for k in range(max(0, t - fs.depth + 1), t + 1):
@@ -684,7 +688,7 @@ def main():
     if rank == 0:
         L = 3
         fsl = K.FrameStream(K_USERS, M_ANT, N_TRAIN, N_DATA, SCHEME, precision="f32", depth=2,
-                            concurrent=True, frames=B)
+                            concurrent=True, frames=B, pilot_labels=True)
         seeds_live = lambda i: [rank * 1_000_000 + 500_000 + i * B + j for j in range(B)]  # noqa: E731
         gen.fill(0, seeds_live(0)).wait()
         torch.cuda.synchronize()
@@ -696,7 +700,7 @@ def main():
                 if i >= 1:
                     fsl.done_event(tick[i - 1]).synchronize()     # slot (i+1)%2 consumed
                 nxt = gen.fill((i + 1) % 2, seeds_live(i + 1))
-            tick.append(fsl.submit(gen.rx[i % 2], gen.pilots[i % 2], gen.tx[i % 2]))
+            tick.append(fsl.submit(gen.rx[i % 2], gen.plab[i % 2], gen.tx[i % 2]))
             if nxt is not None:
                 nxt.wait()
         fsl.done_event(tick[-1]).synchronize()
@@ -805,8 +809,9 @@ def main():
               "cpu_baseline": cpu,
               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                       "d2h_bytes_per_step": int(d2h),
-                      "api": (f"FrameStream(frames={B}, depth=2): pinned host batches, H2D / "
-                              "compute / D2H overlapped across steps"),
+                      "api": (f"FrameStream(frames={B}, depth=2, pilot_labels=True): pinned "
+                              "host batches (rx, pilot labels, payload labels), H2D / compute / "
+                              "D2H overlapped across steps"),
                       "bit_errors_last_step": e2e_bit_err},
               "e2e_live_generation": live,
               "kapsm_bench_rows": harness,

@@ -231,6 +231,16 @@ int kapsm_demap_f32(const float* est, long long n, const float* points, int n_po
 int kapsm_demap_f64(const double* est, long long n, const double* points, int n_points,
                     unsigned char* labels, void* stream);
 
+/* Pilot targets from their constellation labels (the receiver knows the
+ * pilot sequence): targets[2i], targets[2i+1] = points[2 labels[i]],
+ * points[2 labels[i] + 1] for n labels (realified targets, apsm.py:156-169);
+ * a label >= n_points gives NaN targets.  Lets a host ship 1 byte per pilot
+ * and user instead of a complex value (FramePipeline(pilot_labels=True)). */
+int kapsm_targets_from_labels_f32(const unsigned char* labels, long long n, const float* points,
+                                  int n_points, float* targets, void* stream);
+int kapsm_targets_from_labels_f64(const unsigned char* labels, long long n, const double* points,
+                                  int n_points, double* targets, void* stream);
+
 /* Count differing elements of two equal-length streams of elem_bytes (1, 4, 8)
  * wide integers (ber numerator, noma.py:284-292).  *count is accumulated. */
 int kapsm_count_mismatch(const void* a, const void* b, long long n, int elem_bytes,

@@ -83,6 +83,8 @@ SIGNATURES = {
     "kapsm_demap_f32": (_I, [_P, _LL, _P, _I, _P, _P]),
     "kapsm_demap_f64": (_I, [_P, _LL, _P, _I, _P, _P]),
     "kapsm_count_mismatch": (_I, [_P, _P, _LL, _I, _P, _P]),
+    "kapsm_targets_from_labels_f32": (_I, [_P, _LL, _P, _I, _P, _P]),
+    "kapsm_targets_from_labels_f64": (_I, [_P, _LL, _P, _I, _P, _P]),
     # internal instrumentation (not in the public header)
     "kapsm_internal_fp32_peak": (_I, [_P, _I, _I, _P]),
     "kapsm_internal_run_frames_overlap_mode_f32": (_I, [_I, _P, _LL, _P, _P, _I, _I, _I, _I, _I,

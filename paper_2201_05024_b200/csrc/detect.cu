@@ -614,6 +614,43 @@ extern "C" int kapsm_demap_f64(const double* est, long long n, const double* poi
                                int n_points, unsigned char* labels, void* stream) {
   return demap<double>(est, n, points, n_points, labels, (cudaStream_t)stream);
 }
+// Pilot targets from their constellation labels (the receiver knows the
+// pilot sequence; a host that ships labels moves 1 byte per pilot and user
+// instead of a complex value): targets[2i], targets[2i+1] = points[2 labels[i]],
+// points[2 labels[i] + 1], the realified targets of apsm.py:156-169.
+// (a label outside the constellation gives NaN targets)
+template <typename T>
+__global__ void targets_from_labels_kernel(const unsigned char* __restrict__ labels, long long n,
+                                           const T* __restrict__ points, int n_points,
+                                           T* __restrict__ targets) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int l = labels[i];
+  const bool ok = l < n_points;
+  targets[2 * i] = ok ? points[2 * l] : T(NAN);
+  targets[2 * i + 1] = ok ? points[2 * l + 1] : T(NAN);
+}
+template <typename T>
+static int targets_from_labels(const unsigned char* labels, long long n, const T* points,
+                               int n_points, T* targets, void* stream) {
+  if (n < 0 || n_points < 1 || n_points > 64 || (n && (!labels || !points || !targets)))
+    return KAPSM_ERR_INVALID;
+  if (n == 0) return KAPSM_OK;
+  targets_from_labels_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      labels, n, points, n_points, targets);
+  return status_from(cudaGetLastError());
+}
+extern "C" int kapsm_targets_from_labels_f32(const unsigned char* labels, long long n,
+                                             const float* points, int n_points, float* targets,
+                                             void* stream) {
+  return targets_from_labels<float>(labels, n, points, n_points, targets, stream);
+}
+extern "C" int kapsm_targets_from_labels_f64(const unsigned char* labels, long long n,
+                                             const double* points, int n_points, double* targets,
+                                             void* stream) {
+  return targets_from_labels<double>(labels, n, points, n_points, targets, stream);
+}
+
 extern "C" int kapsm_count_mismatch(const void* a, const void* b, long long n, int elem_bytes,
                                     unsigned long long* count, void* stream) {
   if (n < 0 || !count || (n && (!a || !b))) return KAPSM_ERR_INVALID;

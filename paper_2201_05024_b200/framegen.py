@@ -11,6 +11,7 @@ ring that is registered with CUDA as pinned memory:
 * rx      float32 (slots, F, T, M, 2)   interleaved (re, im), pilots first
 * pilots  float32 (slots, F, K, n_train, 2)
 * tx      uint8   (slots, F, K, n_data)  Gray labels of the payload symbols
+* plab    uint8   (slots, F, K, n_train) labels of the pilot symbols
 
 so a slot feeds ``FrameStream.submit`` (H2D by DMA) with no further copy.
 ``fill(slot, seeds)`` starts a slot asynchronously and returns a handle whose
@@ -33,7 +34,7 @@ __all__ = ["FrameGenerator"]
 def _layout(slots, F, K, M, n_train, n_data):
     T = n_train + n_data
     parts = [("rx", (slots, F, T, M, 2), np.float32), ("pilots", (slots, F, K, n_train, 2), np.float32),
-             ("tx", (slots, F, K, n_data), np.uint8)]
+             ("tx", (slots, F, K, n_data), np.uint8), ("plab", (slots, F, K, n_train), np.uint8)]
     off, out = 0, {}
     for name, shape, dt in parts:
         nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
@@ -74,6 +75,7 @@ def _worker_frames(args):
         v["pilots"][slot, i, ..., 0] = pil.real
         v["pilots"][slot, i, ..., 1] = pil.imag
         v["tx"][slot, i] = symbol_labels(fr["bits"][:, nt * k:], k)
+        v["plab"][slot, i] = symbol_labels(fr["bits"][:, :nt * k], k)
     return len(args)
 
 
@@ -115,6 +117,7 @@ class FrameGenerator:
         self.rx = torch.from_numpy(self.views["rx"])
         self.pilots = torch.from_numpy(self.views["pilots"])
         self.tx = torch.from_numpy(self.views["tx"])
+        self.plab = torch.from_numpy(self.views["plab"])      # pilot labels (uint8)
 
     def fill(self, slot: int, seeds: Sequence[int]) -> _Pending:
         """Start generating ``len(seeds) == F`` frames into ``slot``."""
@@ -136,7 +139,7 @@ class FrameGenerator:
             import torch
             torch.cuda.cudart().cudaHostUnregister(self._ptr)
             self.pinned = False
-        self.rx = self.pilots = self.tx = None
+        self.rx = self.pilots = self.tx = self.plab = None
         self.views = None
         try:
             self.shm.close()

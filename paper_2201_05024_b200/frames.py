@@ -38,7 +38,7 @@ class FramePipeline:
     def __init__(self, F: int, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32",
                  store_est: bool = True, device=None, overlap: bool = True,
-                 full_workspace: bool = False):
+                 full_workspace: bool = False, pilot_labels: bool = False):
         if precision not in dv.DTYPES:
             raise ValueError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.cfg = cfg or ApsmConfig()
@@ -64,6 +64,11 @@ class FramePipeline:
         gen = torch.Generator(device=dev).manual_seed(0)
         self.rx.normal_(generator=gen)
         self.pilots = z(F, K, n_train, 2)
+        # pilot_labels: the pilots arrive as constellation labels (uint8,
+        # F x K x n_train) and the launch expands them into the targets on the
+        # device (kapsm_targets_from_labels) -- 1 byte per pilot and user to copy
+        self.pilot_labels = pilot_labels
+        self.pilot_lab = z(F, K, n_train, dt=torch.uint8) if pilot_labels else None
         self.tx = z(F, K, n_data, dt=torch.uint8)
         self.ld = _ld(self.Np)
         # trainer workspace (kapsm_pipeline_workspace_bytes): the pilot Gram +
@@ -115,7 +120,10 @@ class FramePipeline:
                 dst.copy_(torch.from_numpy(np.ascontiguousarray(a)).to(dst.dtype),
                           non_blocking=non_blocking)
         put(self.rx, rx, True)
-        put(self.pilots, pilots, True)
+        if self.pilot_labels:
+            put(self.pilot_lab, pilots, False)
+        else:
+            put(self.pilots, pilots, True)
         put(self.tx, tx_labels, False)
 
     # -- compute ------------------------------------------------------------
@@ -139,7 +147,10 @@ class FramePipeline:
         """Run the pipeline on device-resident inputs in place (no copy into
         the static buffers): tensors shaped and typed like ``rx``/``pilots``/
         ``tx`` (contiguous, same device).  Outputs land in this pipeline's
-        buffers.  Stream-ordered on the current stream; not graph-captured."""
+        buffers.  Stream-ordered on the current stream; not graph-captured.
+        (Complex-target pipelines only: pilot labels go through ``load``.)"""
+        if self.pilot_labels:
+            raise ValueError("launch_on takes target pilots; this pipeline takes pilot labels")
         for name, t, ref in (("rx", rx, self.rx), ("pilots", pilots, self.pilots),
                              ("tx_labels", tx_labels, self.tx)):
             if (not isinstance(t, torch.Tensor) or t.shape != ref.shape or t.dtype != ref.dtype
@@ -166,12 +177,20 @@ class FramePipeline:
         if mode in (2, 3) and int(lib.kapsm_internal_train_tp_ws_bytes(self.F, self.n_train, self.cfg.window)) > \
                 self._gram_buf.numel() * self._gram_buf.element_size():
             raise ValueError("workspace too small for the one-warp trainer")
+        self._expand_pilots()
         _lib.check(_lib.load().kapsm_internal_run_frames_overlap_mode_f32(
             int(mode), *self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
             "run_frames_overlap_mode")
 
+    def _expand_pilots(self):
+        if self.pilot_labels:
+            _lib.check(dv.fn("kapsm_targets_from_labels", self.prec)(
+                dv.ptr(self.pilot_lab), self.pilot_lab.numel(), dv.ptr(self.points),
+                self.n_points, dv.ptr(self.pilots), dv.stream()), "targets_from_labels")
+
     def launch(self):
         """Enqueue the whole pipeline on the current stream."""
+        self._expand_pilots()
         if self.overlap:
             _lib.check(self._fn(*self._args(), dv.stream(), C.c_void_p(self._side.cuda_stream)),
                        "run_frames_overlap")
@@ -258,7 +277,8 @@ class FrameStream:
 
     def __init__(self, K: int, M: int, n_train: int, n_data: int, scheme: str = "QPSK",
                  cfg: Optional[ApsmConfig] = None, precision: str = "f32", depth: int = 2,
-                 device=None, post=None, concurrent: bool = False, frames: int = 1):
+                 device=None, post=None, concurrent: bool = False, frames: int = 1,
+                 pilot_labels: bool = False):
         if depth < 1:
             raise ValueError(f"depth must be >= 1, got {depth}")
         if frames < 1:
@@ -267,8 +287,10 @@ class FrameStream:
         self.depth = depth
         self.frames = frames
         self.pipes = [FramePipeline(frames, K, M, n_train, n_data, scheme, cfg=cfg,
-                                    precision=precision, store_est=False, device=dev)
+                                    precision=precision, store_est=False, device=dev,
+                                    pilot_labels=pilot_labels)
                       for _ in range(depth)]
+        self.pilot_labels = pilot_labels
         for p in self.pipes:
             p.capture()
         torch.cuda.synchronize(dev)
@@ -293,9 +315,10 @@ class FrameStream:
         for k, p in enumerate(self.pipes):
             # with no collectives the slot's "inputs free" point is the graph's end
             comp_ev = self.ev_comp[k] if post is not None else self.ev_end[k]
+            pin_t = p.pilot_lab if pilot_labels else p.pilots
             self._slot.append({
-                "dst_in": VP(p.rx.data_ptr(), p.pilots.data_ptr(), p.tx.data_ptr()),
-                "bytes_in": UL(*(t.numel() * t.element_size() for t in (p.rx, p.pilots, p.tx))),
+                "dst_in": VP(p.rx.data_ptr(), pin_t.data_ptr(), p.tx.data_ptr()),
+                "bytes_in": UL(*(t.numel() * t.element_size() for t in (p.rx, pin_t, p.tx))),
                 "src_in": VP(0, 0, 0),
                 "dst_out": VP4(self.labels_h[k].data_ptr(), self.counts_h[k][0].data_ptr(),
                                self.counts_h[k][1].data_ptr(), self.status_h[k].data_ptr()),
@@ -313,7 +336,8 @@ class FrameStream:
     def submit(self, rx, pilots, tx_labels, start_event=None, timing=None) -> int:
         """Queue one batch of ``frames`` frames (one frame by default): tensors
         shaped like FramePipeline.load's inputs for F = ``frames``
-        (float32/float64 interleaved rx and pilots, uint8 labels), pinned
+        (float32/float64 interleaved rx and pilots -- or uint8 pilot labels
+        with ``pilot_labels`` -- uint8 payload labels), pinned
         host or device-resident; they are copied into the slot's buffers on the
         copy stream and the slot's captured graph runs on its compute stream --
         one library call (``kapsm_stream_frame_in``), results come back with a
@@ -323,7 +347,8 @@ class FrameStream:
         i, slot = self.n, self.n % self.depth
         p = self.pipes[slot]
         sl = self._slot[slot]
-        for t, ref in ((rx, p.rx), (pilots, p.pilots), (tx_labels, p.tx)):
+        for t, ref in ((rx, p.rx), (pilots, p.pilot_lab if self.pilot_labels else p.pilots),
+                       (tx_labels, p.tx)):
             if t.dtype != ref.dtype or t.numel() != ref.numel() or not t.is_contiguous():
                 raise ValueError(f"frame tensor {tuple(t.shape)} {t.dtype} does not match "
                                  f"{tuple(ref.shape)} {ref.dtype}")

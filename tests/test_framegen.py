@@ -5,6 +5,7 @@ byte in the device layout.  CPU only (the ring is not pinned here)."""
 
 import numpy as np
 
+from paper_2201_05024_b200 import get_constellation
 from paper_2201_05024_b200.framegen import FrameGenerator
 from paper_2201_05024_b200.frames import host_frames
 
@@ -21,6 +22,10 @@ def test_generator_matches_host_frames():
         assert np.array_equal(gen.views["rx"][1], ref_rx)
         assert np.array_equal(gen.views["pilots"][1], ref_pil)
         assert np.array_equal(gen.views["tx"][1], tx.astype(np.uint8))
+        # pilot labels: the constellation points of their labels are the pilots
+        pts = get_constellation("QPSK").points
+        assert np.array_equal(pts[gen.views["plab"][1]].astype(np.complex64),
+                              pil.astype(np.complex64))
         # the other slot is untouched (zeros)
         assert not gen.views["rx"][0].any()
         # a second fill of the same slot with other seeds replaces it
@@ -39,5 +44,8 @@ def test_generator_qam16_massive():
         rx, pil, tx, _ = host_frames([3, 4], K, M, nt, nd, "QAM16")
         assert np.array_equal(gen.views["rx"][0], np.stack([rx.real, rx.imag], -1).astype(np.float32))
         assert np.array_equal(gen.views["tx"][0], tx.astype(np.uint8))
+        pts = get_constellation("QAM16").points
+        assert np.array_equal(pts[gen.views["plab"][0]].astype(np.complex64),
+                              pil.astype(np.complex64))
     finally:
         gen.close()

@@ -8,6 +8,7 @@ import glob
 import os
 
 import numpy as np
+import torch
 import pytest
 
 import paper_2201_05024_b200 as K
@@ -460,21 +461,25 @@ def test_launch_on_device_frames_in_place():
         q.launch_on(rx_d.double(), pil_d, tx_d)
 
 
-def test_frame_stream_batches_throughput_mode():
+@pytest.mark.parametrize("labels_in", [False, True])
+def test_frame_stream_batches_throughput_mode(labels_in):
     """FrameStream(frames=F) with F x K > SMs (the bench's e2e path: the
     one-warp trainer inside the captured pipelines), fed from the pinned ring
-    of FrameGenerator: every batch's decisions and counts equal one
-    FramePipeline launch per batch."""
+    of FrameGenerator -- with complex pilot targets, or (the bench's e2e) with
+    pilot labels expanded on the device: every batch's decisions and counts
+    equal one FramePipeline launch per batch on the complex targets."""
     from paper_2201_05024_b200.framegen import FrameGenerator
     F, Kk, M, nt, nd = 30, 6, 16, 200, 160          # 180 chains > 148 SMs
     gen = FrameGenerator(F, Kk, M, nt, nd, "QPSK", slots=2, workers=2)
     try:
-        fs = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=2, concurrent=True, frames=F)
+        fs = K.FrameStream(Kk, M, nt, nd, "QPSK", depth=2, concurrent=True, frames=F,
+                           pilot_labels=labels_in)
         seeds = [list(range(700 + F * b, 700 + F * (b + 1))) for b in range(3)]
         out = []
         for b in range(3):
             gen.fill(b % 2, seeds[b]).wait()
-            t = fs.submit(gen.rx[b % 2], gen.pilots[b % 2], gen.tx[b % 2])
+            t = fs.submit(gen.rx[b % 2], (gen.plab if labels_in else gen.pilots)[b % 2],
+                          gen.tx[b % 2])
             lab, be, se = fs.result(t)
             out.append((lab.clone(), be.clone(), se.clone()))
         for b in range(3):
@@ -488,3 +493,28 @@ def test_frame_stream_batches_throughput_mode():
             assert np.array_equal(out[b][2].numpy(), r["sym_err"])
     finally:
         gen.close()
+
+
+
+def test_pipeline_pilot_labels_equal_targets():
+    """FramePipeline(pilot_labels=True): the targets expanded on the device
+    from the pilot labels (kapsm_targets_from_labels) are the complex targets,
+    bit for bit, and the whole pipeline's outputs are identical."""
+    from paper_2201_05024_b200.noma import seeded_frame, symbol_labels
+    Kk, M, nt, nd, sch = 6, 16, 150, 200, "QAM16"
+    seeds = [41, 42]
+    rx, pil, tx, _ = K.host_frames(seeds, Kk, M, nt, nd, sch)
+    k = 4
+    plab = np.stack([symbol_labels(seeded_frame(s, Kk, M, nt, nd, sch)["bits"][:, :nt * k], k)
+                     for s in seeds]).astype(np.uint8)
+    a = K.FramePipeline(2, Kk, M, nt, nd, sch, precision="f32")
+    a.load(rx, pil, tx)
+    a.launch()
+    b = K.FramePipeline(2, Kk, M, nt, nd, sch, precision="f32", pilot_labels=True)
+    b.load(rx, plab, tx)
+    b.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(a.pilots, b.pilots)
+    ra, rb = a.results(), b.results()
+    for key in ("labels", "bit_err", "n_active", "est", "theta", "coeff"):
+        assert np.array_equal(ra[key], rb[key]), key
