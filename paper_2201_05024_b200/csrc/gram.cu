@@ -32,10 +32,6 @@ __global__ void __launch_bounds__(GRAM_TILE* GRAM_TILE)
                        T w_l, T w_g, T inv2s, T* __restrict__ gram, long long ld,
                        long long gram_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // the trainer launched behind this kernel (programmatic dependent launch)
-  // may start its Gram-independent prologue now; it waits for this grid's
-  // completion before its first Gram read (griddepcontrol.wait)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int rs = 2 * M + 1;                       // odd row stride: conflict-free
   T* xa = reinterpret_cast<T*>(smem_raw);        // [32][rs]
   T* xb = xa + GRAM_T2 * rs;                     // [32][rs]

@@ -341,9 +341,6 @@ __global__ void __launch_bounds__(Roles<NG, CL>::WARPS * 32, 1)
       qsm[2 * i + 1] = ql;
     }
     if (gt < 16) ctl[gt] = 0;
-    // launched as a programmatic dependent of the pilot Gram (pipelines): the
-    // prologue above overlaps it; the Gram is complete and visible past here
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     group_sync();
 
     if (role == NB) {
@@ -914,17 +911,13 @@ int launch_train(int tasks, cudaStream_t s, const T* gram, long long ld, long lo
   cfg.blockDim = dim3(Roles<NG, CL>::WARPS * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  // programmatic dependent launch: the trainer may be scheduled while the
-  // kernel before it on the stream (the pilot Gram) still runs
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(
       &cfg, kern, gram, ld, gram_stride, rx, rx_stride, samples, samples_stride, dim, targets, F,
       K, Np, W, (T)eps, (T)p.w_l, qtab, base0, theta0, coeff, first_step, theta, n_active, status,

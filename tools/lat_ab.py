@@ -7,7 +7,8 @@ import numpy as np, torch
 import paper_2201_05024_b200 as K
 mode = sys.argv[1] if len(sys.argv) > 1 else "fixed"
 rx, pil, tx, _ = K.host_frames(range(64), 6, 16, 685, 3840, "QPSK")
-p = K.FramePipeline(1, 6, 16, 685, 3840, "QPSK", precision="f32", store_est=False)
+p = K.FramePipeline(1, 6, 16, 685, 3840, "QPSK", precision="f32", store_est=False,
+                    overlap="serial" not in sys.argv)
 pool = K.FramePipeline(64, 6, 16, 685, 3840, "QPSK", precision="f32", store_est=False)
 pool.load(rx, pil, tx)
 f0 = int(mode[5:]) if mode.startswith("fixed") and len(mode) > 5 else 0
