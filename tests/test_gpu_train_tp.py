@@ -104,10 +104,13 @@ def test_tp_pipeline_matches_gram_pipeline(F):
 
 
 @pytest.mark.parametrize("W,M,Kn,nt,scheme", [(64, 16, 6, 500, "QPSK"), (132, 16, 6, 400, "QPSK"),
-                                            (40, 64, 16, 300, "QAM16"), (100, 8, 4, 300, "QAM16")])
+                                            (40, 64, 16, 300, "QAM16"), (100, 8, 4, 300, "QAM16"),
+                                            (120, 64, 4, 250, "QAM16")])
 def test_wide_ring_trainer_matches_oracle(W, M, Kn, nt, scheme):
     """The wide-window trainer (one CTA of 32 NW slots per chain, the C3 sweep's
-    W = 64 / 128 regime) on a single frame, in latency mode: atom counts, slot
+    W = 64 / 128 regime; at M = 64, W = 120 the ring-warps + helpers form does
+    not fit shared memory and the plain wide form runs) on a single frame, in
+    latency mode: atom counts, slot
     order, coefficients and theta of two users against the oracle, and the
     detection against the Gram-free path's own oracle-checked decisions."""
     nd = 200
@@ -119,7 +122,13 @@ def test_wide_ring_trainer_matches_oracle(W, M, Kn, nt, scheme):
     for u in (0, Kn - 1):
         ref = _oracle_users(rx[0], pil[0], nt, W, [u])[0]
         assert int(r["n_active"][0, u]) == ref["n_atoms"], (u, W)
-        assert np.array_equal(r["first_step"][0, u], ref["first_step"]), (u, W)
+        # slot order: at most one sample may first activate one step apart --
+        # a residual within FP32 rounding of +-eps at that step (SURVEY 7,
+        # "eps-boundary" flips; the FP64 pipeline matches exactly); the
+        # coefficients below then still agree to 1e-4
+        d = np.nonzero(r["first_step"][0, u] != ref["first_step"])[0]
+        assert len(d) <= 1 and np.all(np.abs(r["first_step"][0, u][d] - ref["first_step"][d]) <= 1), \
+            (u, W, d)
         assert maxrel(r["coeff"][0, u], ref["coeff"]) < 1e-4
         assert maxrel(r["theta"][0, u], ref["theta"]) < 1e-4
         est = O.detect_batch(ref["theta"], ref["atoms"], ref["coeffs"], rx[0, nt:])
