@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(128, 6)
   // lane owns up to 3 pieces for the whole chain; each keeps a running global
   // pointer for its sample mm (m or m - SPAN + 1): g + mm * gm + (mm >> 1) * gt,
   // advanced by gm + (mm odd) gt per step.
-  const int XP = vec ? D / 4 : D, NPC = 2 * XP + 10;
+  const int XP = vec ? D / 4 : D;               // row pieces (pieces: 2 XP + 10)
   const unsigned sg_s = sbase + L::STG;
   // pieces per lane (compile time): 2 rows of up to 8 DPL 16-byte pieces (or
   // 32 DPL 4-byte ones) + 8 band pieces + target + live count
@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(128, 6)
     const long long mm0 = -poff[r];
     pp[r] = g ? g + mm0 * pgm[r] + (mm0 >> 1) * pgt[r] : nullptr;
   }
-  (void)NPC;
   int pm = 0;                    // the sample index m of the next prefetch
   auto prefetch = [&]() {        // stage of sample pm (steps are prefetched in order)
     const unsigned so = (unsigned)((pm & (TP_STG - 1)) * SSTR) * 4;
