@@ -488,6 +488,9 @@ __global__ void __launch_bounds__(256)
   T* Rm = reinterpret_cast<T*>(lsm);            // [32][Dp] this block's rows
   T* Rl = Rm + 32 * Dp;                         // [32][Dp] column tile
   const int f = blockIdx.y, m0 = blockIdx.x * 32;
+  cnt += (long long)f * Np;                     // this frame's rows
+  idx += (long long)f * Np * TW_LCAP;
+  val += (long long)f * Np * TW_LCAP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const T* X = rx ? rx + (long long)f * rx_stride : nullptr;
   const T* Sm = rx ? nullptr : samples + (long long)f * samples_stride;

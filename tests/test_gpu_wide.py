@@ -173,3 +173,24 @@ def test_large_np_latency_trainer_f64_vs_oracle():
     f = K.train(None, zip(fr["rx"][:n_train], fr["symbols"][u, :n_train]), K.ApsmConfig(),
                 precision="f64")
     _check(f, O.train_user(R, B, W=20))
+
+
+@pytest.mark.parametrize("F,Kn,M,nt,W", [(2, 2, 2, 100, 25), (3, 2, 4, 100, 25), (2, 8, 2, 160, 40)])
+def test_general_trainer_multi_frame_live_lists(F, Kn, M, nt, W):
+    """FP64 pipelines of several frames at small M (many live Gaussian terms:
+    the general trainer's per-frame live lists are used and overflow) against
+    the oracle, every frame: coefficients and theta to 1e-9.  (Regression: the
+    lists of frames >= 1 were written over frame 0's.)"""
+    from oracle import kapsm_oracle as O
+    seeds = list(range(100, 100 + F))
+    rx, pil, tx, _ = K.host_frames(seeds, Kn, M, nt, 50, "QPSK")
+    p = K.FramePipeline(F, Kn, M, nt, 50, "QPSK", cfg=K.ApsmConfig(window=W), precision="f64")
+    p.load(rx, pil, tx)
+    p.launch()
+    r = p.results()
+    for f in range(F):
+        for u in (0, Kn - 1):
+            ref = O.train_user(O.realify(rx[f, :nt]), O.realify_targets(pil[f, u]), W=W)
+            assert int(r["n_active"][f, u]) == ref["n_atoms"], (f, u)
+            assert np.max(np.abs(r["coeff"][f, u] - ref["coeff"])) <= 1e-9 * np.max(np.abs(ref["coeff"]))
+            assert np.max(np.abs(r["theta"][f, u] - ref["theta"])) <= 1e-9 * np.max(np.abs(ref["theta"]))
