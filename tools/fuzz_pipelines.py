@@ -24,11 +24,20 @@ for case in range(n_cases):
         p.load(rx, pil, tx); p.launch()
         out[prec] = p.results()
     a, b = out["f32"], out["f64"]
+    # user 0 / frame F-1 against the oracle (both precisions)
+    from oracle import kapsm_oracle as O
+    f = F - 1
+    ref = O.train_user(O.realify(rx[f, :nt]), O.realify_targets(pil[f, 0]), W=W)
+    est = O.detect_batch(ref["theta"], ref["atoms"], ref["coeffs"], rx[f, nt:])
+    o_err = max(np.max(np.abs(out[pr]["est"][f, 0] - est)) / max(1e-30, np.max(np.abs(est)))
+                for pr in ("f32", "f64"))
+    o_lab = max(np.mean(out[pr]["labels"][f, 0] != O.demap_indices(est, sch)) for pr in ("f32", "f64"))
     lab_mis = np.mean(a["labels"] != b["labels"])
     at_mis = np.mean(a["n_active"] != b["n_active"])
     est_rel = np.max(np.abs(a["est"] - b["est"])) / max(1e-30, np.max(np.abs(b["est"])))
-    ok = lab_mis <= 1e-3 and est_rel < 1e-3
+    ok = lab_mis <= 1e-3 and est_rel < 1e-3 and o_err < 1e-3 and o_lab <= 1e-2
     bad += not ok
     print(f"case {case}: F={F} K={Kn} M={M} {sch} nt={nt} nd={nd} W={W}: label mismatch {lab_mis:.2e}, "
-          f"atoms mismatch {at_mis:.2f}, est rel {est_rel:.1e} {'OK' if ok else 'BAD'}", flush=True)
+          f"atoms mismatch {at_mis:.2f}, est rel {est_rel:.1e}, vs oracle est {o_err:.1e} labels {o_lab:.1e} "
+          f"{'OK' if ok else 'BAD'}", flush=True)
 print("bad cases:", bad)
