@@ -1108,13 +1108,34 @@ __global__ void __launch_bounds__(32 * (NW + TPL_NH), 1)
       if constexpr (decltype(dl_on)::value) {
         const float4* dd4 = reinterpret_cast<const float4*>(dcur);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-        {
+        if constexpr (NW == 1) {
           // the whole ring, unrolled and branch-free (deltas outside the
           // window are zero, K is finite everywhere): every load can be in
           // flight at once, at (R - W - P) / R extra shared-memory traffic
 #pragma unroll
           for (int k = 0; k < R / 4; k += 2) {
             const float4 d0 = dd4[k], k0 = kk4[k], d1 = dd4[k + 1], k1 = kk4[k + 1];
+            a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
+            a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
+            a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
+            a3 = ffma2(make_float2(d1.z, d1.w), make_float2(k1.z, k1.w), a3);
+          }
+        } else {
+          // wide rings: K only over the 8-slot groups the window [n-W+1, n]
+          // touches (a rotating run of the ring); the other groups hold zero
+          // deltas, so the sum is unchanged.
+          constexpr int G = R / 8;
+          int sw = sn - (W - 1);
+          sw += sw < 0 ? R : 0;                  // slot of the oldest window sample
+          const int g0 = sw >> 3, ng = ((sw & 7) + W + 7) >> 3;
+          unsigned gm = ng >= G ? 0xffffffffu : (1u << ng) - 1u;
+          gm = ng >= G ? gm : ((gm << g0) | (gm >> (G - g0)));
+#pragma unroll
+          for (int k = 0; k < R / 4; k += 2) {
+            // outside the window: K's chunk is replaced by the (zero) delta
+            // chunk itself -- a broadcast read, 1 wavefront instead of 4
+            const float4* kr = ((gm >> (k >> 1)) & 1u) ? kk4 : dd4;
+            const float4 d0 = dd4[k], k0 = kr[k], d1 = dd4[k + 1], k1 = kr[k + 1];
             a0 = ffma2(make_float2(d0.x, d0.y), make_float2(k0.x, k0.y), a0);
             a1 = ffma2(make_float2(d0.z, d0.w), make_float2(k0.z, k0.w), a1);
             a2 = ffma2(make_float2(d1.x, d1.y), make_float2(k1.x, k1.y), a2);
