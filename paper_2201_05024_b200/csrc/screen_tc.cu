@@ -458,14 +458,21 @@ __global__ void __launch_bounds__(TC_THREADS)
     int j = 0;
     if (t < n_data) {
       const int pmax = t + list_max_off;
-      for (int w = 0; w < NW && w * 32 <= pmax; ++w) {
-        unsigned b = bits[w * BST + r];
-        while (b) {
-          const int pp = w * 32 + __ffs(b) - 1;
-          b &= b - 1;
-          if (pp > pmax) break;
-          if (j < TC_CAP) lp[r * TC_CAP + j] = pp;
-          ++j;
+      const int nwl = pmax < 0 ? 0 : min(NW, pmax / 32 + 1);   // words with w * 32 <= pmax
+      for (int w0 = 0; w0 < nwl; w0 += 8) {
+        unsigned bw[8];                     // 8 words in flight, then their bits
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bw[k] = w0 + k < nwl ? bits[(w0 + k) * BST + r] : 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          unsigned b = bw[k];
+          while (b) {
+            const int pp = (w0 + k) * 32 + __ffs(b) - 1;
+            b &= b - 1;
+            if (pp > pmax) break;
+            if (j < TC_CAP) lp[r * TC_CAP + j] = pp;
+            ++j;
+          }
         }
       }
       cnt[(long long)f * n_data + t] = j <= TC_CAP ? j : -1;
