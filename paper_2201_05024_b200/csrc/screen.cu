@@ -348,13 +348,29 @@ __global__ void __launch_bounds__(256)
     T gr = T(0), gi = T(0);
     if (tvalid && w_g != T(0) && nl >= 0) {                 // the screen's compact list
       const float4* vt = vals + ((long long)f * n_data + t) * SC_CAP;
-      for (int j = 0; j < nl; ++j) {
-        const float4 vv = vt[j];
-        const int p = __float_as_int(vv.w);
-        const T c1 = cu[2 * p], c2 = cu[2 * p + 1];
-        const T ka = (T)vv.x, kb = (T)vv.y, kc = (T)vv.z;
-        gr = fma(c1, ka, fma(c2, kc, gr));
-        gi = fma(c1, kb, fma(c2, ka, gi));
+      // entries 4 at a time: the list loads, then the coefficient loads they
+      // index, in flight together (two memory round trips per 4 entries
+      // instead of two per entry); accumulated in list order as before
+      for (int j0 = 0; j0 < nl; j0 += 4) {
+        float4 vv[4];
+        T c1[4], c2[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          vv[i] = j0 + i < nl ? vt[j0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int p = __float_as_int(vv[i].w);
+          c1[i] = j0 + i < nl ? cu[2 * p] : T(0);
+          c2[i] = j0 + i < nl ? cu[2 * p + 1] : T(0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (j0 + i < nl) {
+            const T ka = (T)vv[i].x, kb = (T)vv[i].y, kc = (T)vv[i].z;
+            gr = fma(c1[i], ka, fma(c2[i], kc, gr));
+            gi = fma(c1[i], kb, fma(c2[i], ka, gi));
+          }
+        }
       }
     } else if (tvalid && w_g != T(0)) {                     // too many live pilots: recompute
       const unsigned* lf = live + (long long)f * NW * n_data + t;
