@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < PER; ++i) {
       const int e = 4 * (tid + i * nthr);
       if (e < n) {
-        const int r = e / rl, c = e - r * rl;
+        // rows of exactly 2 MT floats (M == MT): a shift, not a division
+        const int r = rl == 2 * MT ? e / (2 * MT) : e / rl, c = e - r * rl;
         T* d = buf + r * YS + c;
         d[0] = (T)v[i].x; d[1] = (T)v[i].y; d[2] = (T)v[i].z; d[3] = (T)v[i].w;
       }
