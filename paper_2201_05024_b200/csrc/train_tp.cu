@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256)
     const int q4 = D / 4, n4 = (r1 - r0) * q4;
     const float4* src = reinterpret_cast<const float4*>(X + (long long)r0 * D);
     for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-      const int r = i / q4, c = i - r * q4;
+      const int r = q4 == 8 ? i / 8 : i / q4, c = i - r * q4;      // (M = 16: a shift)
       *reinterpret_cast<float4*>(rows + r * DS + 4 * c) = __ldg(src + i);
     }
   } else {
@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(256)
   const int pairs = TT * (H + 1);
   const bool gauss = w_g != 0.f;
   for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-    const int tt = i / (H + 1), dt = i - tt * (H + 1), t = t0 + tt, tp = t - dt;
+    // (the one-warp ring's R = 32: a division by a constant)
+    const int tt = H == 16 ? i / 17 : i / (H + 1), dt = i - tt * (H + 1), t = t0 + tt, tp = t - dt;
     if (t >= n_train) continue;
     float vals[2][2] = {{0.f, 0.f}, {0.f, 0.f}};          // [alpha][beta]
     if (tp >= 0) {
