@@ -162,7 +162,15 @@ __global__ void __launch_bounds__(256)
         a0 = xr + yi; a1 = xi - yr;
         ec = fmaf(a0, a0, fmaf(a1, a1, ec));
       };
-      if ((D & 3) == 0) {
+      if (D == 32) {                          // 16 antennas: unrolled
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 xv = *reinterpret_cast<const float4*>(x + 4 * q);
+          const float4 yv = *reinterpret_cast<const float4*>(y + 4 * q);
+          acc(xv.x, xv.y, yv.x, yv.y);
+          acc(xv.z, xv.w, yv.z, yv.w);
+        }
+      } else if ((D & 3) == 0) {
         for (int q = 0; q < D / 4; ++q) {
           const float4 xv = *reinterpret_cast<const float4*>(x + 4 * q);
           const float4 yv = *reinterpret_cast<const float4*>(y + 4 * q);
