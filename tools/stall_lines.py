@@ -7,10 +7,10 @@ d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
 cubin = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout.split("\n")
-sec = None; cur = "?"; a2l = {}
+sec = None; cur = "?"; a2l = {}; nsec = 0
 for l in dis:
     if l.strip().startswith(".section") and ".text." in l:
-        sec = sym in l; continue
+        sec = sym in l; nsec += sec; continue
     if not sec: continue
     if "//##" in l:
         m = re.search(r'File "([^"]+)", line (\d+)', l)
@@ -18,6 +18,8 @@ for l in dis:
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
     if m: a2l[int(m.group(1), 16)] = cur
+if nsec != 1:      # offsets are per function: several matches would mix their line maps
+    sys.exit(f"{nsec} functions match {sym!r}: pass a substring of one mangled name")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hi_ = [i for i, r in enumerate(rows) if "Instructions Executed" in r][0]
