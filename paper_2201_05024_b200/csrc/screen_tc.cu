@@ -481,9 +481,12 @@ __global__ void __launch_bounds__(TC_THREADS)
   }
   __syncthreads();
   for (int it = tid; it < NT * TC_CAP; it += TC_THREADS) {
-    const int r = it / TC_CAP, j = it - r * TC_CAP;
+    // entry-major: the first entries of all NT symbols go to NT different
+    // threads (lists are short: symbol-major put a symbol's entries, and
+    // every eighth symbol, on one thread, one memory round trip after another)
+    const int j = it / NT, r = it - j * NT;
     if (j >= lnum[r]) continue;
-    const int t = t0 + r, pp = lp[it];
+    const int t = t0 + r, pp = lp[r * TC_CAP + j];
     const float* x = Xf + (long long)pp * D;
     const float* y = Yf + (long long)t * D;
     float ea = 0.f, eb = 0.f, ec = 0.f;
