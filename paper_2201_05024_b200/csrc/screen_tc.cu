@@ -270,9 +270,8 @@ __global__ void __launch_bounds__(TC_THREADS)
     // ---- transposed form: MMA M = 128 payload symbols (A = their rows, then
     //      their rotations), N = 128 pilots (B = the pilot tile) -> TMEM lane =
     //      symbol, column = pilot: Re c in columns 0..127, Im c in 128..255.
-    //      A thread tests its symbol against 32 pilots per TMEM load with one
-    //      OR-accumulated compare per pair; the live word is assembled only in
-    //      the rare chunks that have a live pair. ----
+    //      A thread tests its symbol against 32 pilots per TMEM load and
+    //      builds their live word in the same pass. ----
     const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(128 >> 3) << 17) |
                            ((unsigned)(128 >> 4) << 24);
     const int sym = 32 * q + lane;                                 // this thread's symbol
@@ -337,20 +336,13 @@ __global__ void __launch_bounds__(TC_THREADS)
         for (int k = 0; k < 8; ++k) th4[k] = lds_f4(smem_u32(ath + pb + 4 * k));
         tmem_wait_ld();
         const float* thp = reinterpret_cast<const float*>(th4);
-        bool any = false;
+        // the word in one pass: a warp meets a live pair in most chunks (32
+        // symbols x 32 pilots), so an any-test + rebuild pass costs more
+        unsigned w = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
-          any |= m > thp[j] + bsym;
-        }
-        unsigned w = 0;
-        if (__builtin_expect(any, false)) {   // rare: keep it a branch, not predicated code
-          asm volatile("" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float m = fmaxf(__uint_as_float(re[j]), fabsf(__uint_as_float(im[j])));
-            w |= (m > thp[j] + bsym ? 1u : 0u) << j;
-          }
+          w |= m > thp[j] + bsym ? (1u << j) : 0u;
         }
         const int wrd = (mt * TC_MROWS + pb) >> 5;
         if (wrd < NW && (!GB || t0 + sym < n_data)) bits[wrd * BST + sym] = w;
